@@ -1,0 +1,158 @@
+/*
+ * tk_b200.h -- C ABI of the B200 (sm_100a) CT-operator library (libtkb200.so).
+ *
+ * Drop-in boundary for the reference's projector kernel layer
+ * (/root/reference/pkg/src/tomokit/_kernels.py) and its FFT row filter
+ * (/root/reference/pkg/src/tomokit/filters.py).  Conventions follow the
+ * reference exactly (see _kernels.py:9-16, grids.py:8-11):
+ *   - world coordinate of index i on an axis with n samples, spacing s:
+ *     (i - (n-1)/2) * s ; volumes are C-order (y,x) / (z,y,x);
+ *     sinograms (view,u) / (view,v,u) with u the fastest axis;
+ *   - forward operators integrate the zero-extended bi/trilinear interpolant
+ *     with midpoint sampling at `step` (last partial step exact), in value*mm;
+ *   - back operators are voxel-driven linear/bilinear gathers, optionally
+ *     weighted by (sid/w)^2.
+ *
+ * Memory: every float* grid argument is a DEVICE pointer (fp32, C-contiguous).
+ * Per-view geometry (angles as cos/sin, projection matrices, sources, M^-1) is
+ * passed as HOST float64 arrays -- exactly the arrays the reference computes on
+ * the host (projectors.py:106-248) -- and packed/uploaded by the library.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  All calls are
+ * stream-ordered and asynchronous with respect to the host; scratch memory is
+ * stream-ordered (cudaMallocAsync) and released before return.  Outputs are
+ * fully overwritten (unless an `accumulate` flag says otherwise); inputs are
+ * never modified.  Unlike the reference, volumes are passed UNPADDED: the
+ * one-voxel zero margin of projectors.py:26-29 is applied inside the library.
+ *
+ * Every function returns 0 on success, TK_ERR_ARG for an invalid argument,
+ * TK_ERR_CUDA for a CUDA error; tk_last_error() returns the thread's message.
+ */
+#ifndef TK_B200_H
+#define TK_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_OK 0
+#define TK_ERR_ARG 1
+#define TK_ERR_CUDA 2
+
+/* Library identity and diagnostics. */
+int tk_version(void);                 /* major*10000 + minor*100 + patch */
+const char *tk_last_error(void);      /* thread-local; "" when no error */
+int tk_device_info(int *sm_major, int *sm_minor, int *sm_count);
+/* Number of kernel launches issued by this library since load (all threads). */
+unsigned long long tk_launch_count(void);
+
+/* ---- parallel-beam 2D ------------------------------------------------------
+ * replaces _kernels.forward_parallel_2d (_kernels.py:160-171), called from
+ * projectors.forward_project_parallel_2d (projectors.py:106-123).
+ * vol (ny,nx) device; cos_a/sin_a host float64[n_ang]; out (n_ang,n_det). */
+int tk_forward_parallel_2d(const float *vol, int ny, int nx, double sy, double sx,
+                           const double *cos_a, const double *sin_a, int n_ang,
+                           int n_det, double ds, double step, float *out,
+                           void *stream);
+/* replaces _kernels.back_parallel_2d (_kernels.py:174-195),
+ * projectors.back_project_parallel_2d (projectors.py:126-142). */
+int tk_back_parallel_2d(const float *sino, int n_ang, int n_det,
+                        const double *cos_a, const double *sin_a, double ds,
+                        int ny, int nx, double sy, double sx, float *out,
+                        void *stream);
+
+/* ---- fan-beam 2D -----------------------------------------------------------
+ * replaces _kernels.forward_fan_2d (_kernels.py:198-216). */
+int tk_forward_fan_2d(const float *vol, int ny, int nx, double sy, double sx,
+                      const double *cos_a, const double *sin_a, int n_ang,
+                      double sdd, double sid, int n_det, double ds, double step,
+                      float *out, void *stream);
+/* replaces _kernels.back_fan_2d (_kernels.py:219-251). */
+int tk_back_fan_2d(const float *sino, int n_ang, int n_det, const double *cos_a,
+                   const double *sin_a, double sdd, double sid, double ds, int ny,
+                   int nx, double sy, double sx, int weighted, float *out,
+                   void *stream);
+
+/* ---- cone-beam 3D ----------------------------------------------------------
+ * replaces _kernels.forward_cone_3d (_kernels.py:254-278) as called from
+ * projectors.forward_project_cone_3d (projectors.py:205-225).
+ * vol (nz,ny,nx) device; sources host float64 (V,3); minv host float64 (V,3,3)
+ * (= projectors._cone_rays, projectors.py:191-202); out (V,rows,cols). */
+int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz,
+                       double sy, double sx, const double *sources,
+                       const double *minv, int n_views, int rows, int cols,
+                       double step, float *out, void *stream);
+/* replaces _kernels.back_cone_3d (_kernels.py:281-322) as called from
+ * projectors.back_project_cone_3d (projectors.py:228-248).
+ * sino (V,rows,cols) device; mats host float64 (V,3,4); out (nz,ny,nx). */
+int tk_back_cone_3d(const float *sino, int n_views, int rows, int cols,
+                    const double *mats, double sid, int weighted, int nz, int ny,
+                    int nx, double sz, double sy, double sx, float *out,
+                    void *stream);
+/* Sharded variant of tk_back_cone_3d (no reference counterpart; multi-GPU
+ * z-slab / view-chunk decomposition).  Computes the voxels with global z index
+ * in [z_begin, z_begin+z_count) of the (nz,ny,nx) grid into out (z_count,ny,nx),
+ * reading a detector row band: `sino` holds rows [row_begin, row_begin+band_rows)
+ * of every view (V, band_rows, cols); rows outside the band read as zero.
+ * accumulate != 0 adds into out instead of overwriting it. */
+int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols,
+                       int row_begin, int band_rows, const double *mats,
+                       double sid, int weighted, int nz, int ny, int nx,
+                       double sz, double sy, double sx, int z_begin, int z_count,
+                       int accumulate, float *out, void *stream);
+
+/* ---- matched adjoints (exact transposes; not in the reference, which pairs
+ * A with the unmatched voxel-driven B, autodiff.py:1-19) ------------------------
+ * Scatter kernels (fp32 atomics: results are deterministic only up to fp32
+ * summation order).  out is overwritten. */
+int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int cols,
+                               const double *sources, const double *minv,
+                               int nz, int ny, int nx, double sz, double sy,
+                               double sx, double step, float *vol_out,
+                               void *stream);
+int tk_back_cone_3d_adjoint(const float *vol, int nz, int ny, int nx, double sz,
+                            double sy, double sx, const double *mats, double sid,
+                            int weighted, int n_views, int rows, int cols,
+                            float *sino_out, void *stream);
+int tk_forward_parallel_2d_adjoint(const float *sino, int n_ang, int n_det,
+                                   const double *cos_a, const double *sin_a,
+                                   double ds, double step, int ny, int nx,
+                                   double sy, double sx, float *vol_out,
+                                   void *stream);
+int tk_forward_fan_2d_adjoint(const float *sino, int n_ang, int n_det,
+                              const double *cos_a, const double *sin_a,
+                              double sdd, double sid, double ds, double step,
+                              int ny, int nx, double sy, double sx, float *vol_out,
+                              void *stream);
+
+/* ---- FFT row filter (filters.py:136-171, 204-211) ---------------------------
+ * For each of n_rows rows of `width` samples (row r belongs to detector row
+ * (r % det_rows)): optional obliquity pre-weight sdd/sqrt(sdd^2+u^2+v^2)
+ * (u,v metric detector offsets with pitches du,dv; disabled when sdd <= 0),
+ * zero-pad to n_pad (power of two >= 2*width), multiply DFT bin k by
+ * half_weights[min(k, n_pad-k)] (host float64[n_pad/2+1]), inverse transform,
+ * crop to width and scale by `scale` (the filter's detector_spacing).
+ * in and out may alias. */
+int tk_fft_filter_rows(const float *in, long long n_rows, int width, int det_rows,
+                       const double *half_weights, int n_pad, double scale,
+                       double sdd, double du, double dv, float *out,
+                       void *stream);
+
+/* Row-band variant for z-slab sharding: the buffer holds `band_rows` detector
+ * rows starting at detector row `row_offset` of a `det_rows`-row detector
+ * (buffer row r is detector row (r % band_rows) + row_offset, which sets the v
+ * coordinate of the pre-weight). */
+int tk_fft_filter_rows_ex(const float *in, long long n_rows, int width, int band_rows,
+                          int row_offset, int det_rows, const double *half_weights,
+                          int n_pad, double scale, double sdd, double du, double dv,
+                          float *out, void *stream);
+
+/* ---- helpers --------------------------------------------------------------- */
+/* out[i] = in[i] * scale (fp32), n elements; in/out may alias. */
+int tk_scale(const float *in, long long n, double scale, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TK_B200_H */

@@ -1,0 +1,62 @@
+// tk_common.cuh -- shared helpers for the sm_100a CT-operator kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/tk_b200.h"
+
+namespace tk {
+
+// Reference constant _TINY (_kernels.py:24).
+constexpr double kTiny = 1e-12;
+
+// ---- error plumbing (thread-local message, int status) ----------------------
+void set_error(const std::string &msg);
+void clear_error();
+int fail_arg(const std::string &msg);
+int check_cuda(cudaError_t e, const char *what);
+void count_launch(unsigned n = 1);
+
+#define TK_TRY_CUDA(expr)                                  \
+  do {                                                     \
+    cudaError_t _e = (expr);                               \
+    if (_e != cudaSuccess) return ::tk::check_cuda(_e, #expr); \
+  } while (0)
+
+// Check the last launch and count it.
+#define TK_LAUNCHED(name)                                         \
+  do {                                                            \
+    cudaError_t _e = cudaGetLastError();                          \
+    if (_e != cudaSuccess) return ::tk::check_cuda(_e, name);     \
+    ::tk::count_launch();                                         \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
+struct Scratch {
+  void *ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  Scratch() = default;
+  Scratch(const Scratch &) = delete;
+  Scratch &operator=(const Scratch &) = delete;
+  cudaError_t alloc(size_t bytes, cudaStream_t s);
+  ~Scratch();
+  template <class T> T *as() const { return reinterpret_cast<T *>(ptr); }
+};
+
+// Upload a host array to fresh stream-ordered scratch.
+cudaError_t upload(Scratch &dst, const void *host, size_t bytes, cudaStream_t s);
+
+inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+int sm_count();
+
+// ---- device helpers ---------------------------------------------------------
+__device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
+
+}  // namespace tk

@@ -1,0 +1,604 @@
+// tk_cone.cu -- cone-beam 3D forward (ray-driven) and back (voxel-driven)
+// projectors for sm_100a, plus their exact transposes (matched adjoints).
+//
+// Semantics follow the reference kernels line for line
+// (/root/reference/pkg/src/tomokit/_kernels.py:117-157, 254-322); the
+// arithmetic is reorganised for the GPU:
+//   * forward: per-ray set-up (direction M^-1 (c,r,1), normalisation, slab
+//     clipping, sample count) in float64; the march itself in float32 in
+//     padded-index space, sample k at  e + (k + 1/2) * g  computed directly
+//     (no accumulated t), exact last partial segment.
+//   * back: projection-matrix rows are pre-multiplied by the voxel spacing,
+//     shifted by the detector centre (principal-point shift keeps fp32 well
+//     conditioned), and evaluated on centred integer voxel coordinates.  For
+//     trajectories whose detector column/depth rows have no z component
+//     (circular, helical, sinusoidal orbits with v = +z) the column, depth and
+//     distance weight are computed once per (x,y,view) and reused by ZB voxels
+//     along z; only the row coordinate advances.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "tk_common.cuh"
+
+namespace tk {
+
+struct ConeRayView {  // per-view forward constants (float64): source, M^-1
+  double src[3];
+  double minv[9];
+};
+
+struct ConeVoxView {  // per-view back constants (float32), see pack_bp_views
+  float a[4];  // column numerator (principal-point shifted)
+  float b[4];  // row numerator (principal-point shifted)
+  float w[4];  // depth
+};
+
+// ---------------------------------------------------------------------------
+// zero-padded copy: volp (nz+2, ny+2, nx+2)  <-  vol (nz, ny, nx)
+// (reference projectors.py:26-29)
+// ---------------------------------------------------------------------------
+__global__ void pad3d_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
+                             float *__restrict__ volp) {
+  const int nxp = nx + 2, nyp = ny + 2, nzp = nz + 2;
+  const long long total = (long long)nzp * nyp * nxp;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x = (int)(i % nxp);
+    long long t = i / nxp;
+    int y = (int)(t % nyp);
+    int z = (int)(t / nyp);
+    float v = 0.f;
+    if (x >= 1 && x <= nx && y >= 1 && y <= ny && z >= 1 && z <= nz)
+      v = __ldg(vol + ((long long)(z - 1) * ny + (y - 1)) * nx + (x - 1));
+    volp[i] = v;
+  }
+}
+
+// crop a padded fp32 volume back to (nz, ny, nx)
+__global__ void crop3d_kernel(const float *__restrict__ volp, int nz, int ny, int nx,
+                              float *__restrict__ vol) {
+  const long long total = (long long)nz * ny * nx;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x = (int)(i % nx);
+    long long t = i / nx;
+    int y = (int)(t % ny);
+    int z = (int)(t / ny);
+    vol[i] = volp[((long long)(z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + (x + 1)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ray set-up shared by the forward projector and its transpose.
+// Returns false when the ray misses the box (reference _clip_ray_3d, t0 >= t1).
+// ---------------------------------------------------------------------------
+struct RaySetup {
+  float ex, ey, ez;  // padded-index coordinates of the clip entry point
+  float gx, gy, gz;  // padded-index increment per full step
+  int n;             // number of samples (reference loop count)
+  float last;        // fraction of a step covered by the last sample (0,1]
+};
+
+__device__ __forceinline__ bool clip_axis(double p, double d, double h, double &t0,
+                                          double &t1) {
+  if (fabs(d) > kTiny) {
+    double ta = (-h - p) / d, tb = (h - p) / d;
+    t0 = fmax(t0, fmin(ta, tb));
+    t1 = fmin(t1, fmax(ta, tb));
+    return true;
+  }
+  return !(p < -h || p > h);
+}
+
+__device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int c, int nx,
+                                               int ny, int nz, double sx, double sy,
+                                               double sz, double step, RaySetup &rs) {
+  // _kernels.py:262-265
+  double dx = V.minv[0] * c + V.minv[1] * r + V.minv[2];
+  double dy = V.minv[3] * c + V.minv[4] * r + V.minv[5];
+  double dz = V.minv[6] * c + V.minv[7] * r + V.minv[8];
+  double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  dx *= inv;
+  dy *= inv;
+  dz *= inv;
+  const double px = V.src[0], py = V.src[1], pz = V.src[2];
+  // _kernels.py:125-130 (_clip_ray_3d on the half-extents (n+1) s / 2)
+  double t0 = -1e300, t1 = 1e300;
+  if (!clip_axis(px, dx, (nx + 1) * sx / 2.0, t0, t1)) return false;
+  if (!clip_axis(py, dy, (ny + 1) * sy / 2.0, t0, t1)) return false;
+  if (!clip_axis(pz, dz, (nz + 1) * sz / 2.0, t0, t1)) return false;
+  if (!(t0 < t1)) return false;
+  // _kernels.py:133: while t < t1 - TINY  ->  n = ceil((t1 - TINY - t0) / step)
+  double span = (t1 - kTiny - t0) / step;
+  if (!(span > 0.0)) return false;
+  int n = (int)ceil(span);
+  double last = (t1 - t0) / step - (double)(n - 1);
+  if (last > 1.0) last = 1.0;
+  // padded-index coordinates (centre (n-1)/2 + 1, _kernels.py:122-124, 138-140)
+  const double cx = (nx - 1) / 2.0 + 1.0, cy = (ny - 1) / 2.0 + 1.0, cz = (nz - 1) / 2.0 + 1.0;
+  rs.ex = (float)((px + t0 * dx) / sx + cx);
+  rs.ey = (float)((py + t0 * dy) / sy + cy);
+  rs.ez = (float)((pz + t0 * dz) / sz + cz);
+  rs.gx = (float)(step * dx / sx);
+  rs.gy = (float)(step * dy / sy);
+  rs.gz = (float)(step * dz / sz);
+  rs.n = n;
+  rs.last = (float)last;
+  return true;
+}
+
+// One trilinear sample of the zero-padded volume at padded-index coordinates
+// (_kernels.py:141-154).  Returns 0 outside 0 <= i < n+1.
+__device__ __forceinline__ float trilinear_padded(const float *__restrict__ volp, int nxp,
+                                                  int nyp, int nzp, float fx, float fy,
+                                                  float fz) {
+  const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
+  if ((unsigned)ix >= (unsigned)(nxp - 1) || (unsigned)iy >= (unsigned)(nyp - 1) ||
+      (unsigned)iz >= (unsigned)(nzp - 1))
+    return 0.f;
+  const float wx = fx - flx, wy = fy - fly, wz = fz - flz;
+  const unsigned sxy = (unsigned)nyp * (unsigned)nxp;
+  const float *p = volp + ((unsigned)iz * sxy + (unsigned)iy * (unsigned)nxp + (unsigned)ix);
+  const float *q = p + sxy;
+  const float v00 = lerpf(__ldg(p), __ldg(p + 1), wx);
+  const float v01 = lerpf(__ldg(p + nxp), __ldg(p + nxp + 1), wx);
+  const float v10 = lerpf(__ldg(q), __ldg(q + 1), wx);
+  const float v11 = lerpf(__ldg(q + nxp), __ldg(q + nxp + 1), wx);
+  return lerpf(lerpf(v00, v01, wy), lerpf(v10, v11, wy), wz);
+}
+
+// ---------------------------------------------------------------------------
+// Forward projection: one thread per detector pixel; a warp covers an 8x4
+// pixel tile so its rays sample a compact patch of the volume at each step.
+// ---------------------------------------------------------------------------
+constexpr int kFpBX = 8, kFpBY = 16;
+
+__global__ void __launch_bounds__(kFpBX *kFpBY)
+    cone_fp_kernel(const float *__restrict__ volp, int nx, int ny, int nz, double sx,
+                   double sy, double sz, const ConeRayView *__restrict__ views, int rows,
+                   int cols, double step, float *__restrict__ out) {
+  const int c = blockIdx.x * kFpBX + threadIdx.x;
+  const int r = blockIdx.y * kFpBY + threadIdx.y;
+  const int v = blockIdx.z;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const ConeRayView V = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(V, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  const int nxp = nx + 2, nyp = ny + 2, nzp = nz + 2;
+  float acc = 0.f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k) {
+    const float kf = (float)k + 0.5f;
+    acc += trilinear_padded(volp, nxp, nyp, nzp, fmaf(kf, rs.gx, rs.ex),
+                            fmaf(kf, rs.gy, rs.ey), fmaf(kf, rs.gz, rs.ez));
+  }
+  {  // last (possibly partial) segment, midpoint at t + seg/2
+    const float kf = (float)nfull + 0.5f * rs.last;
+    acc += rs.last * trilinear_padded(volp, nxp, nyp, nzp, fmaf(kf, rs.gx, rs.ex),
+                                      fmaf(kf, rs.gy, rs.ey), fmaf(kf, rs.gz, rs.ez));
+  }
+  *dst = acc * (float)step;
+}
+
+// Exact transpose of cone_fp_kernel: scatter y * seg * weights into the padded
+// accumulation volume (fp32 atomics).
+__device__ __forceinline__ void trilinear_scatter(float *__restrict__ adjp, int nxp, int nyp,
+                                                  int nzp, float fx, float fy, float fz,
+                                                  float g) {
+  const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
+  if ((unsigned)ix >= (unsigned)(nxp - 1) || (unsigned)iy >= (unsigned)(nyp - 1) ||
+      (unsigned)iz >= (unsigned)(nzp - 1))
+    return;
+  const float wx = fx - flx, wy = fy - fly, wz = fz - flz;
+  const unsigned sxy = (unsigned)nyp * (unsigned)nxp;
+  float *p = adjp + ((unsigned)iz * sxy + (unsigned)iy * (unsigned)nxp + (unsigned)ix);
+  float *q = p + sxy;
+  const float gz0 = g * (1.f - wz), gz1 = g * wz;
+  const float a0 = gz0 * (1.f - wy), a1 = gz0 * wy, b0 = gz1 * (1.f - wy), b1 = gz1 * wy;
+  atomicAdd(p, a0 * (1.f - wx));
+  atomicAdd(p + 1, a0 * wx);
+  atomicAdd(p + nxp, a1 * (1.f - wx));
+  atomicAdd(p + nxp + 1, a1 * wx);
+  atomicAdd(q, b0 * (1.f - wx));
+  atomicAdd(q + 1, b0 * wx);
+  atomicAdd(q + nxp, b1 * (1.f - wx));
+  atomicAdd(q + nxp + 1, b1 * wx);
+}
+
+__global__ void __launch_bounds__(kFpBX *kFpBY)
+    cone_fp_adjoint_kernel(const float *__restrict__ sino, int nx, int ny, int nz,
+                           double sx, double sy, double sz,
+                           const ConeRayView *__restrict__ views, int rows, int cols,
+                           double step, float *__restrict__ adjp) {
+  const int c = blockIdx.x * kFpBX + threadIdx.x;
+  const int r = blockIdx.y * kFpBY + threadIdx.y;
+  const int v = blockIdx.z;
+  if (c >= cols || r >= rows) return;
+  const float y = __ldg(sino + ((long long)v * rows + r) * cols + c);
+  if (y == 0.f) return;
+  const ConeRayView V = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(V, r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
+  const int nxp = nx + 2, nyp = ny + 2, nzp = nz + 2;
+  const float g = y * (float)step;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k) {
+    const float kf = (float)k + 0.5f;
+    trilinear_scatter(adjp, nxp, nyp, nzp, fmaf(kf, rs.gx, rs.ex), fmaf(kf, rs.gy, rs.ey),
+                      fmaf(kf, rs.gz, rs.ez), g);
+  }
+  const float kf = (float)nfull + 0.5f * rs.last;
+  trilinear_scatter(adjp, nxp, nyp, nzp, fmaf(kf, rs.gx, rs.ex), fmaf(kf, rs.gy, rs.ey),
+                    fmaf(kf, rs.gz, rs.ez), g * rs.last);
+}
+
+// ---------------------------------------------------------------------------
+// Back projection (voxel-driven gather), _kernels.py:281-322.
+// Thread = one (x, y) column and ZB consecutive z voxels; loop over views
+// with the per-view constants staged in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kBpBX = 32, kBpBY = 8, kBpChunk = 128;
+
+struct BpParams {
+  const float *sino;
+  long long view_stride;  // elements between views of the (band) sinogram
+  int n_views, band_rows, cols;
+  const ConeVoxView *views;
+  float cu, cv;  // column / row shift constants (cv already minus row_begin)
+  float sid;
+  int nx, ny, z_begin, z_count;
+  float cx, cy, cz;  // volume centre (index units)
+  int accumulate;
+  float *out;
+};
+
+// Column taps (clamped indices + weights, zero outside [0, cols)).
+__device__ __forceinline__ void col_taps(float fc, int cols, int &ca, int &cb, float &g0,
+                                         float &g1) {
+  const float fl = floorf(fc);
+  const int c0 = (int)fl;
+  const float wc = fc - fl;
+  g0 = ((unsigned)c0 < (unsigned)cols) ? 1.f - wc : 0.f;
+  g1 = ((unsigned)(c0 + 1) < (unsigned)cols) ? wc : 0.f;
+  ca = min(max(c0, 0), cols - 1);
+  cb = min(max(c0 + 1, 0), cols - 1);
+}
+
+template <int ZB, bool ZINV, bool WEIGHTED>
+__global__ void __launch_bounds__(kBpBX *kBpBY) cone_bp_kernel(const BpParams p) {
+  __shared__ ConeVoxView sv[kBpChunk];
+  const int ix = blockIdx.x * kBpBX + threadIdx.x;
+  const int iy = blockIdx.y * kBpBY + threadIdx.y;
+  const int zl0 = blockIdx.z * ZB;  // local z of this thread's first voxel
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx;
+  const float yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  const int tid = threadIdx.y * kBpBX + threadIdx.x;
+
+  float acc[ZB];
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) acc[k] = 0.f;
+
+  for (int v0 = 0; v0 < p.n_views; v0 += kBpChunk) {
+    const int nch = min(kBpChunk, p.n_views - v0);
+    __syncthreads();
+    for (int i = tid; i < nch * 12; i += kBpBX * kBpBY)
+      reinterpret_cast<float *>(sv)[i] = __ldg(reinterpret_cast<const float *>(p.views + v0) + i);
+    __syncthreads();
+    if (!active) continue;
+    for (int j = 0; j < nch; ++j) {
+      const ConeVoxView &V = sv[j];
+      const float *s = p.sino + (long long)(v0 + j) * p.view_stride;
+      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+      if (ZINV) {
+        if (!(w0 > (float)kTiny)) continue;  // _kernels.py:297-298
+        const float rw = 1.f / w0;
+        int ca, cb;
+        float g0, g1;
+        col_taps(fmaf(a0, rw, p.cu), p.cols, ca, cb, g0, g1);
+        if (WEIGHTED) {  // (sid / w)^2 folded into the column weights
+          const float q = p.sid * rw;
+          g0 *= q * q;
+          g1 *= q * q;
+        }
+        if (g0 == 0.f && g1 == 0.f) continue;
+        const float fr0 = fmaf(b0, rw, p.cv);
+        const float dr = V.b[2] * rw;
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float fl = floorf(fr);
+          const int r0 = (int)fl;
+          const float wr = fr - fl;
+          const float h0 = ((unsigned)r0 < (unsigned)p.band_rows) ? 1.f - wr : 0.f;
+          const float h1 = ((unsigned)(r0 + 1) < (unsigned)p.band_rows) ? wr : 0.f;
+          const int ra = min(max(r0, 0), p.band_rows - 1);
+          const int rb = min(max(r0 + 1, 0), p.band_rows - 1);
+          const float *sa = s + (long long)ra * p.cols;
+          const float *sb = s + (long long)rb * p.cols;
+          const float top = fmaf(g0, __ldg(sa + ca), g1 * __ldg(sa + cb));
+          const float bot = fmaf(g0, __ldg(sb + ca), g1 * __ldg(sb + cb));
+          acc[k] = fmaf(h0, top, fmaf(h1, bot, acc[k]));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float kf = (float)k;
+          const float w = fmaf(kf, V.w[2], w0);
+          if (!(w > (float)kTiny)) continue;
+          const float rw = 1.f / w;
+          int ca, cb;
+          float g0, g1;
+          col_taps(fmaf(fmaf(kf, V.a[2], a0), rw, p.cu), p.cols, ca, cb, g0, g1);
+          const float fr = fmaf(fmaf(kf, V.b[2], b0), rw, p.cv);
+          const float fl = floorf(fr);
+          const int r0 = (int)fl;
+          const float wr = fr - fl;
+          const float h0 = ((unsigned)r0 < (unsigned)p.band_rows) ? 1.f - wr : 0.f;
+          const float h1 = ((unsigned)(r0 + 1) < (unsigned)p.band_rows) ? wr : 0.f;
+          const int ra = min(max(r0, 0), p.band_rows - 1);
+          const int rb = min(max(r0 + 1, 0), p.band_rows - 1);
+          const float *sa = s + (long long)ra * p.cols;
+          const float *sb = s + (long long)rb * p.cols;
+          float val = h0 * fmaf(g0, __ldg(sa + ca), g1 * __ldg(sa + cb)) +
+                      h1 * fmaf(g0, __ldg(sb + ca), g1 * __ldg(sb + cb));
+          if (WEIGHTED) {
+            const float q = p.sid * rw;
+            val *= q * q;
+          }
+          acc[k] += val;
+        }
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
+// Exact transpose of the (unweighted or weighted) voxel-driven back projector:
+// splat each voxel into the detector with the same bilinear weights.
+__global__ void __launch_bounds__(256)
+    cone_bp_adjoint_kernel(const float *__restrict__ vol, int nx, int ny, int nz, float cx,
+                           float cy, float cz, const ConeVoxView *__restrict__ views,
+                           int n_views, int rows, int cols, float cu, float cv, float sid,
+                           int weighted, float *__restrict__ sino) {
+  const long long nvox = (long long)nx * ny * nz;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (i >= nvox) return;
+  const float g = __ldg(vol + i);
+  if (g == 0.f) return;
+  const int ix = (int)(i % nx), iy = (int)((i / nx) % ny), iz = (int)(i / ((long long)nx * ny));
+  const float xc = (float)ix - cx, yc = (float)iy - cy, zc = (float)iz - cz;
+  const ConeVoxView V = views[v];
+  const float w = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc, V.w[3])));
+  if (!(w > (float)kTiny)) return;
+  const float rw = 1.f / w;
+  const float fc = fmaf(fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc, V.a[3]))), rw, cu);
+  const float fr = fmaf(fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc, V.b[3]))), rw, cv);
+  float gg = g;
+  if (weighted) {
+    const float q = sid * rw;
+    gg *= q * q;
+  }
+  const float flc = floorf(fc), flr = floorf(fr);
+  const int c0 = (int)flc, r0 = (int)flr;
+  const float wc = fc - flc, wr = fr - flr;
+  float *s = sino + (long long)v * rows * cols;
+  if ((unsigned)r0 < (unsigned)rows) {
+    if ((unsigned)c0 < (unsigned)cols) atomicAdd(s + (long long)r0 * cols + c0, gg * (1.f - wr) * (1.f - wc));
+    if ((unsigned)(c0 + 1) < (unsigned)cols) atomicAdd(s + (long long)r0 * cols + c0 + 1, gg * (1.f - wr) * wc);
+  }
+  if ((unsigned)(r0 + 1) < (unsigned)rows) {
+    if ((unsigned)c0 < (unsigned)cols) atomicAdd(s + (long long)(r0 + 1) * cols + c0, gg * wr * (1.f - wc));
+    if ((unsigned)(c0 + 1) < (unsigned)cols) atomicAdd(s + (long long)(r0 + 1) * cols + c0 + 1, gg * wr * wc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side packing
+// ---------------------------------------------------------------------------
+
+// Fold voxel spacing into P and shift the column/row rows by the detector
+// centre: a' = (P0 - cu P2) . (s * (i - c), 1) etc., so fc = cu + a'/w.
+static void pack_bp_views(const double *mats, int n_views, double sx, double sy, double sz,
+                          double cu, double cv, std::vector<ConeVoxView> &out, bool &zinv) {
+  out.resize(n_views);
+  zinv = true;
+  for (int i = 0; i < n_views; ++i) {
+    const double *P = mats + 12 * i;
+    const double s[3] = {sx, sy, sz};
+    ConeVoxView &V = out[i];
+    for (int j = 0; j < 3; ++j) {
+      V.a[j] = (float)((P[j] - cu * P[8 + j]) * s[j]);
+      V.b[j] = (float)((P[4 + j] - cv * P[8 + j]) * s[j]);
+      V.w[j] = (float)(P[8 + j] * s[j]);
+    }
+    V.a[3] = (float)(P[3] - cu * P[11]);
+    V.b[3] = (float)(P[7] - cv * P[11]);
+    V.w[3] = (float)P[11];
+    if (V.a[2] != 0.f || V.w[2] != 0.f) zinv = false;
+  }
+}
+
+static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double sy,
+                     double sx, const double *sources, const double *minv, int n_views,
+                     int rows, int cols, double step, float *out, cudaStream_t st,
+                     bool adjoint) {
+  std::vector<ConeRayView> hv(n_views);
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].minv[j] = minv[9 * i + j];
+  }
+  Scratch dviews, volp;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
+  const long long npad = (long long)(nz + 2) * (ny + 2) * (nx + 2);
+  TK_TRY_CUDA(volp.alloc(sizeof(float) * npad, st));
+  const unsigned pgrid = (unsigned)std::min<long long>(ceil_div(npad, 256), 148LL * 32);
+  dim3 block(kFpBX, kFpBY);
+  dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
+  if (!adjoint) {
+    pad3d_kernel<<<pgrid, 256, 0, st>>>(vol, nz, ny, nx, volp.as<float>());
+    TK_LAUNCHED("pad3d_kernel");
+    cone_fp_kernel<<<grid, block, 0, st>>>(volp.as<float>(), nx, ny, nz, sx, sy, sz,
+                                           dviews.as<ConeRayView>(), rows, cols, step, out);
+    TK_LAUNCHED("cone_fp_kernel");
+  } else {
+    // here `vol` is the sinogram and `out` the volume
+    TK_TRY_CUDA(cudaMemsetAsync(volp.ptr, 0, sizeof(float) * npad, st));
+    cone_fp_adjoint_kernel<<<grid, block, 0, st>>>(vol, nx, ny, nz, sx, sy, sz,
+                                                   dviews.as<ConeRayView>(), rows, cols,
+                                                   step, volp.as<float>());
+    TK_LAUNCHED("cone_fp_adjoint_kernel");
+    const long long nv = (long long)nz * ny * nx;
+    crop3d_kernel<<<(unsigned)std::min<long long>(ceil_div(nv, 256), 148LL * 32), 256, 0, st>>>(
+        volp.as<float>(), nz, ny, nx, out);
+    TK_LAUNCHED("crop3d_kernel");
+  }
+  return TK_OK;
+}
+
+template <int ZB, bool ZINV>
+static void launch_bp_t(const BpParams &p, bool weighted, dim3 grid, dim3 block,
+                        cudaStream_t st) {
+  if (weighted)
+    cone_bp_kernel<ZB, ZINV, true><<<grid, block, 0, st>>>(p);
+  else
+    cone_bp_kernel<ZB, ZINV, false><<<grid, block, 0, st>>>(p);
+}
+
+}  // namespace tk
+
+using namespace tk;
+
+extern "C" {
+
+int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz, double sy,
+                       double sx, const double *sources, const double *minv, int n_views,
+                       int rows, int cols, double step, float *out, void *stream) {
+  clear_error();
+  if (!vol || !out || !sources || !minv) return fail_arg("tk_forward_cone_3d: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_forward_cone_3d: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0 && step > 0)) return fail_arg("tk_forward_cone_3d: spacing/step must be > 0");
+  if (n_views > 65535) return fail_arg("tk_forward_cone_3d: more than 65535 views per call");
+  return launch_fp(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out,
+                   as_stream(stream), false);
+}
+
+int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int cols,
+                               const double *sources, const double *minv, int nz, int ny,
+                               int nx, double sz, double sy, double sx, double step,
+                               float *vol_out, void *stream) {
+  clear_error();
+  if (!sino || !vol_out || !sources || !minv) return fail_arg("tk_forward_cone_3d_adjoint: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_forward_cone_3d_adjoint: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0 && step > 0)) return fail_arg("tk_forward_cone_3d_adjoint: spacing/step must be > 0");
+  if (n_views > 65535) return fail_arg("tk_forward_cone_3d_adjoint: more than 65535 views per call");
+  return launch_fp(sino, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step,
+                   vol_out, as_stream(stream), true);
+}
+
+int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int row_begin,
+                       int band_rows, const double *mats, double sid, int weighted, int nz,
+                       int ny, int nx, double sz, double sy, double sx, int z_begin,
+                       int z_count, int accumulate, float *out, void *stream) {
+  clear_error();
+  if (!sino || !out || !mats) return fail_arg("tk_back_cone_3d: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_back_cone_3d: non-positive extent");
+  if (band_rows < 1 || row_begin < 0 || row_begin + band_rows > rows)
+    return fail_arg("tk_back_cone_3d: row band outside the detector");
+  if (z_count < 1 || z_begin < 0 || z_begin + z_count > nz)
+    return fail_arg("tk_back_cone_3d: z range outside the volume");
+  if (!(sx > 0 && sy > 0 && sz > 0)) return fail_arg("tk_back_cone_3d: spacing must be > 0");
+  cudaStream_t st = as_stream(stream);
+  const double cu = (cols - 1) / 2.0, cv = (rows - 1) / 2.0;
+  std::vector<ConeVoxView> hv;
+  bool zinv = true;
+  pack_bp_views(mats, n_views, sx, sy, sz, cu, cv, hv, zinv);
+  Scratch dviews;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeVoxView) * n_views, st));
+  BpParams p;
+  p.sino = sino;
+  p.view_stride = (long long)band_rows * cols;
+  p.n_views = n_views;
+  p.band_rows = band_rows;
+  p.cols = cols;
+  p.views = dviews.as<ConeVoxView>();
+  p.cu = (float)cu;
+  p.cv = (float)(cv - row_begin);
+  p.sid = (float)sid;
+  p.nx = nx;
+  p.ny = ny;
+  p.z_begin = z_begin;
+  p.z_count = z_count;
+  p.cx = (float)((nx - 1) / 2.0);
+  p.cy = (float)((ny - 1) / 2.0);
+  p.cz = (float)((nz - 1) / 2.0);
+  p.accumulate = accumulate;
+  p.out = out;
+  constexpr int ZB = 8;
+  dim3 block(kBpBX, kBpBY);
+  dim3 grid(ceil_div(nx, kBpBX), ceil_div(ny, kBpBY), ceil_div(z_count, ZB));
+  if (zinv)
+    launch_bp_t<ZB, true>(p, weighted != 0, grid, block, st);
+  else
+    launch_bp_t<ZB, false>(p, weighted != 0, grid, block, st);
+  TK_LAUNCHED("cone_bp_kernel");
+  return TK_OK;
+}
+
+int tk_back_cone_3d(const float *sino, int n_views, int rows, int cols, const double *mats,
+                    double sid, int weighted, int nz, int ny, int nx, double sz, double sy,
+                    double sx, float *out, void *stream) {
+  return tk_back_cone_3d_ex(sino, n_views, rows, cols, 0, rows, mats, sid, weighted, nz, ny,
+                            nx, sz, sy, sx, 0, nz, 0, out, stream);
+}
+
+int tk_back_cone_3d_adjoint(const float *vol, int nz, int ny, int nx, double sz, double sy,
+                            double sx, const double *mats, double sid, int weighted,
+                            int n_views, int rows, int cols, float *sino_out, void *stream) {
+  clear_error();
+  if (!vol || !sino_out || !mats) return fail_arg("tk_back_cone_3d_adjoint: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_back_cone_3d_adjoint: non-positive extent");
+  if (n_views > 65535) return fail_arg("tk_back_cone_3d_adjoint: more than 65535 views per call");
+  cudaStream_t st = as_stream(stream);
+  const double cu = (cols - 1) / 2.0, cv = (rows - 1) / 2.0;
+  std::vector<ConeVoxView> hv;
+  bool zinv = true;
+  pack_bp_views(mats, n_views, sx, sy, sz, cu, cv, hv, zinv);
+  Scratch dviews;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeVoxView) * n_views, st));
+  TK_TRY_CUDA(cudaMemsetAsync(sino_out, 0, sizeof(float) * (size_t)n_views * rows * cols, st));
+  const long long nvox = (long long)nx * ny * nz;
+  dim3 grid(ceil_div(nvox, 256), n_views);
+  cone_bp_adjoint_kernel<<<grid, 256, 0, st>>>(vol, nx, ny, nz, (float)((nx - 1) / 2.0),
+                                               (float)((ny - 1) / 2.0), (float)((nz - 1) / 2.0),
+                                               dviews.as<ConeVoxView>(), n_views, rows, cols,
+                                               (float)cu, (float)cv, (float)sid, weighted,
+                                               sino_out);
+  TK_LAUNCHED("cone_bp_adjoint_kernel");
+  return TK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,372 @@
+"""GPU parity: the sm_100a kernels against the reference's golden vectors and the
+float64 C oracle, within the north-star tolerance (relative L2 <= 1e-4).
+
+All calls go through libtkb200.so (the C ABI); nothing here falls back to CPU.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north star: relative L2 <= 1e-4 on sinograms and volumes
+
+
+def rel(got, want):
+    got = np.asarray(got.detach().cpu().numpy() if isinstance(got, torch.Tensor) else got, np.float64)
+    want = np.asarray(want, np.float64)
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def tk(cuda):
+    import paper_2511_08427_b200 as tk
+
+    return tk
+
+
+def T(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float32)).cuda()
+
+
+# ---------------------------------------------------------------------------
+# golden vectors (produced by the reference itself)
+# ---------------------------------------------------------------------------
+
+
+class TestGolden:
+    def test_parallel(self, tk, golden):
+        g = golden("parallel2d")
+        geom = tk.GeometryParallel2D((32, 32), (1.0, 1.0), 48, 1.0, g["angles"])
+        assert rel(tk.forward_project(tk.Volume(g["x"], (1, 1)), geom).data, g["fp"]) < TOL
+        assert rel(tk.forward_project(tk.Volume(g["sl"], (1, 1)), geom).data, g["fp_sl"]) < TOL
+        assert rel(tk.forward_project(tk.Volume(g["x"], (1, 1)), geom, tk.SamplingConfig(1.0)).data,
+                   g["fp_step1"]) < TOL
+        assert rel(tk.back_project(tk.Sinogram(g["y"], (1.0,)), geom).data, g["bp"]) < TOL
+        g2 = tk.GeometryParallel2D((20, 28), (0.7, 1.3), 37, 0.9, g["angles2"])
+        assert rel(tk.forward_project(tk.Volume(g["x2"], (0.7, 1.3)), g2).data, g["fp2"]) < TOL
+        assert rel(tk.back_project(tk.Sinogram(g["y2"], (0.9,)), g2).data, g["bp2"]) < TOL
+        assert rel(tk.fbp_parallel_2d(tk.Sinogram(g["y"], (1.0,)), geom, "shepp_logan").data, g["fbp"]) < TOL
+        assert rel(tk.fbp_parallel_2d(tk.Sinogram(g["y"], (1.0,)), geom, "ramp").data, g["fbp_ramp"]) < TOL
+
+    def test_fan(self, tk, golden):
+        g = golden("fan2d")
+        geom = tk.GeometryFan2D((32, 32), (1.0, 1.0), 64, 1.6, g["angles"], sdd=1200.0, sid=750.0)
+        assert rel(tk.forward_project(tk.Volume(g["x"], (1, 1)), geom).data, g["fp"]) < TOL
+        y = tk.Sinogram(g["y"], (1.6,))
+        assert rel(tk.back_project(y, geom).data, g["bp"]) < TOL
+        assert rel(tk.back_project(y, geom, fdk_weighting=True).data, g["bpw"]) < TOL
+        assert rel(tk.fbp_fan_2d(y, geom, "cosine").data, g["fbp"]) < TOL
+
+    def test_cone(self, tk, golden):
+        g = golden("cone3d")
+        geom = tk.circular_cone_geometry((16, 16, 16), (1, 1, 1), (12, 12), (1.6, 1.6), 8, 2 * np.pi,
+                                         1200.0, 750.0)
+        assert rel(tk.forward_project(tk.Volume(g["x"], (1, 1, 1)), geom).data, g["fp"]) < TOL
+        assert rel(tk.forward_project(tk.Volume(g["sl"], (1, 1, 1)), geom).data, g["fp_sl"]) < TOL
+        y = tk.Sinogram(g["y"], (1.6, 1.6))
+        assert rel(tk.back_project(y, geom).data, g["bp"]) < TOL
+        assert rel(tk.back_project(y, geom, True).data, g["bpw"]) < TOL
+        assert rel(tk.filter_stage(y, geom, "shepp_logan").data, g["filt"]) < TOL
+        assert rel(tk.fdk_cone_3d(y, geom, "shepp_logan").data, g["fdk"]) < TOL
+
+    def test_cone_helical_and_tilted(self, tk, golden):
+        g = golden("cone3d_general")
+        gh = tk.GeometryCone3D((14, 18, 16), (1.1, 0.9, 1.0), (10, 14), (1.5, 1.8),
+                               [tk.ProjectionMatrix(m) for m in g["mats_helix"]], 1200.0, 750.0)
+        assert rel(tk.forward_project(tk.Volume(g["xh"], (1.1, 0.9, 1.0)), gh).data, g["fp_h"]) < TOL
+        assert rel(tk.back_project(tk.Sinogram(g["yh"], (1.5, 1.8)), gh, True).data, g["bp_h"]) < TOL
+        gt = tk.GeometryCone3D((12, 12, 12), (1, 1, 1), (12, 12), (1.6, 1.6),
+                               [tk.ProjectionMatrix(m) for m in g["mats_tilt"]], 1200.0, 750.0)
+        assert rel(tk.forward_project(tk.Volume(g["xt"], (1, 1, 1)), gt).data, g["fp_t"]) < TOL
+        assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
+
+
+# ---------------------------------------------------------------------------
+# C-oracle parity at larger sizes
+# ---------------------------------------------------------------------------
+
+
+def cone(tk, n, det, ds, views, spacing=1.0, sdd=1200.0, sid=750.0):
+    return tk.circular_cone_geometry((n, n, n), (spacing,) * 3, (det, det), (ds, ds), views, 2 * np.pi,
+                                     sdd, sid)
+
+
+class TestOracle:
+    def test_cone_fp_bp_64(self, tk, oracle):
+        geom = cone(tk, 64, 96, 1.6, 40)
+        x = oracle.shepp_logan_3d((64, 64, 64)) + 0.1 * np.random.default_rng(1).standard_normal((64,) * 3)
+        mats = geom.matrix_array()
+        fp = tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data
+        assert rel(fp, oracle.forward_cone_3d(x, (1, 1, 1), mats, (96, 96), 0.5)) < TOL
+        y = np.random.default_rng(2).standard_normal((40, 96, 96))
+        for w in (False, True):
+            bp = tk.back_project(tk.Sinogram(y, (1.6, 1.6)), geom, w).data
+            assert rel(bp, oracle.back_cone_3d(y, mats, 750.0, (64,) * 3, (1, 1, 1), w)) < TOL
+
+    def test_fdk_128_shepp_logan(self, tk, oracle):
+        # the survey's fp32 precision probe: 128^3 @1mm, 256^2 @(400/256, 600/256) mm, 180 views
+        n = 128
+        geom = tk.circular_cone_geometry((n,) * 3, (1, 1, 1), (256, 256), (400 / 256, 600 / 256), 180,
+                                         2 * np.pi, 1200.0, 750.0)
+        x = oracle.shepp_logan_3d((n,) * 3)
+        mats = geom.matrix_array()
+        sino = oracle.forward_cone_3d(x, (1, 1, 1), mats, (256, 256), 0.5)
+        want = oracle.fdk_cone_3d(sino, mats, 1200.0, 750.0, (400 / 256, 600 / 256), (n,) * 3, (1, 1, 1),
+                                  "shepp_logan")
+        got = tk.fdk_cone_3d(tk.Sinogram(sino, (400 / 256, 600 / 256)), geom, "shepp_logan").data
+        assert rel(got, want) < TOL
+        got_fp = tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data
+        assert rel(got_fp, sino) < TOL
+
+    def test_cfg4_view_subset(self, tk, oracle):
+        """Headline geometry (512^3 @0.5 mm, 1024^2 @0.6 mm) on 4 views spread over
+        the 720-view orbit, full detector resolution."""
+        full = tk.circular_cone_geometry((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6), 720, 2 * np.pi,
+                                         1200.0, 750.0)
+        mats = full.matrix_array()[::180]
+        geom = tk.GeometryCone3D((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6),
+                                 [tk.ProjectionMatrix(m) for m in mats], 1200.0, 750.0)
+        x = tk.phantoms.shepp_logan_3d((512,) * 3)
+        xh = x.cpu().numpy().astype(np.float64)
+        fp = tk.forward_project(tk.Volume(x, (0.5,) * 3), geom).data
+        want = oracle.forward_cone_3d(xh, (0.5,) * 3, mats, (1024, 1024), 0.25)
+        assert rel(fp, want) < TOL
+        filt = oracle.filter_stage_cone(want, 1200.0, 750.0, (0.6, 0.6), "shepp_logan")
+        bp = tk.back_project(tk.Sinogram(filt, (0.6, 0.6)), geom, True).data
+        assert rel(bp, oracle.back_cone_3d(filt, mats, 750.0, (512,) * 3, (0.5,) * 3, True)) < TOL
+
+    def test_2d_larger(self, tk, oracle):
+        ang = tk.circular_trajectory_2d(180, np.pi)
+        gp = tk.GeometryParallel2D((256, 256), (1.0, 1.0), 367, 1.0, ang)
+        x = np.random.default_rng(3).standard_normal((256, 256))
+        assert rel(tk.forward_project(tk.Volume(x, (1, 1)), gp).data,
+                   oracle.forward_parallel_2d(x, (1, 1), ang, 367, 1.0, 0.5)) < TOL
+        angf = tk.circular_trajectory_2d(360, 2 * np.pi)
+        gf = tk.GeometryFan2D((512, 512), (1.0, 1.0), 768, 1.6, angf, sdd=1200.0, sid=750.0)
+        x = np.random.default_rng(4).standard_normal((512, 512))
+        assert rel(tk.forward_project(tk.Volume(x, (1, 1)), gf).data,
+                   oracle.forward_fan_2d(x, (1, 1), angf, 1200.0, 750.0, 768, 1.6, 0.5)) < TOL
+        y = np.random.default_rng(5).standard_normal((360, 768))
+        assert rel(tk.back_project(tk.Sinogram(y, (1.6,)), gf, True).data,
+                   oracle.back_fan_2d(y, angf, 1200.0, 750.0, 1.6, (512, 512), (1, 1), True)) < TOL
+
+    def test_edge_cases(self, tk, oracle):
+        # ragged sizes, detector larger / smaller than the volume shadow, odd extents
+        geom = tk.GeometryCone3D((7, 9, 5), (0.8, 1.3, 0.9), (3, 17), (2.5, 0.7),
+                                 tk.circular_trajectory_3d(5, 1.3, 1200.0, 750.0, (3, 17), (2.5, 0.7)),
+                                 1200.0, 750.0)
+        rng = np.random.default_rng(9)
+        x = rng.standard_normal((7, 9, 5))
+        mats = geom.matrix_array()
+        st = 0.5 * 0.8
+        assert rel(tk.forward_project(tk.Volume(x, (0.8, 1.3, 0.9)), geom).data,
+                   oracle.forward_cone_3d(x, (0.8, 1.3, 0.9), mats, (3, 17), st)) < TOL
+        y = rng.standard_normal((5, 3, 17))
+        assert rel(tk.back_project(tk.Sinogram(y, (2.5, 0.7)), geom, True).data,
+                   oracle.back_cone_3d(y, mats, 750.0, (7, 9, 5), (0.8, 1.3, 0.9), True)) < TOL
+        # a single view, a single detector row
+        g1 = tk.circular_cone_geometry((16, 16, 16), (1, 1, 1), (1, 40), (1.0, 1.0), 1, 2 * np.pi, 1200.0, 750.0)
+        x = rng.standard_normal((16, 16, 16))
+        assert rel(tk.forward_project(tk.Volume(x, (1, 1, 1)), g1).data,
+                   oracle.forward_cone_3d(x, (1, 1, 1), g1.matrix_array(), (1, 40), 0.5)) < TOL
+
+    def test_zero_in_zero_out(self, tk):
+        geom = cone(tk, 16, 12, 1.6, 6)
+        assert not tk.forward_project(tk.Volume(np.zeros((16,) * 3), (1, 1, 1)), geom).data.any()
+        assert not tk.back_project(tk.Sinogram(np.zeros((6, 12, 12)), (1.6, 1.6)), geom, True).data.any()
+        assert not tk.fdk_cone_3d(tk.Sinogram(np.zeros((6, 12, 12)), (1.6, 1.6)), geom).data.any()
+
+
+# ---------------------------------------------------------------------------
+# analytic known-answer tests (reference test_projectors.py:64-163)
+# ---------------------------------------------------------------------------
+
+
+class TestChords:
+    def test_cone_central_ray(self, tk):
+        geom = tk.circular_cone_geometry((128,) * 3, (1, 1, 1), (25, 25), (2.0, 2.0), 1, 2 * np.pi, 1200.0, 750.0)
+        ball = tk.phantoms.ball_phantom((128,) * 3, 40.0)
+        sino = tk.forward_project(tk.Volume(ball, (1, 1, 1)), geom, tk.SamplingConfig(1.0)).data
+        assert abs(float(sino[0, 12, 12]) - 80.0) <= 2.0
+
+    def test_parallel_random_offsets(self, tk, rng):
+        shape, sp = (256, 256), (0.5, 0.5)
+        disk = tk.phantoms.disk_phantom(shape, 40.0, 1.0, sp)
+        angles = rng.uniform(0, 2 * np.pi, 100)
+        geom = tk.GeometryParallel2D(shape, sp, 181, 0.45, angles)
+        sino = tk.forward_project(tk.Volume(disk, sp), geom, tk.SamplingConfig(1.0)).data.cpu().numpy()
+        offsets = (np.arange(181) - 90) * 0.45
+        js = np.clip(rng.integers(0, 160, 100) + 10, 10, 170)
+        for i in range(100):
+            expected = 2 * np.sqrt(max(40.0**2 - offsets[js[i]] ** 2, 0.0))
+            assert abs(sino[i, js[i]] - expected) <= 1.0
+
+
+# ---------------------------------------------------------------------------
+# matched adjoints and autograd
+# ---------------------------------------------------------------------------
+
+
+class TestAdjoint:
+    def test_cone_matched_dot_test(self, tk):
+        geom = cone(tk, 32, 24, 2.0, 20, spacing=0.9)
+        op = tk.forward_projection_op(geom, matched=True)
+        assert tk.dot_test(op, trials=4) <= 1e-4
+        opb = tk.back_projection_op(geom, matched=True)
+        assert tk.dot_test(opb, trials=4) <= 1e-4
+
+    def test_2d_matched_dot_test(self, tk):
+        ang = tk.circular_trajectory_2d(90, 2 * np.pi)
+        gp = tk.GeometryParallel2D((64, 64), (0.5, 0.5), 96, 0.8, ang)
+        gf = tk.GeometryFan2D((64, 64), (1, 1), 96, 1.1, ang, sdd=1200.0, sid=750.0)
+        for g in (gp, gf):
+            assert tk.dot_test(tk.forward_projection_op(g, matched=True), trials=4) <= 1e-4
+
+    def test_matched_equals_oracle_transpose(self, tk, oracle):
+        geom = cone(tk, 12, 10, 1.7, 5)
+        y = np.random.default_rng(11).standard_normal((5, 10, 10))
+        got = tk.transpose_forward_project(tk.Sinogram(y, (1.7, 1.7)), geom).data
+        want = oracle.forward_cone_3d_T(y, (12,) * 3, (1, 1, 1), geom.matrix_array(), 0.5)
+        assert rel(got, want) < TOL
+        x = np.random.default_rng(12).standard_normal((12,) * 3)
+        got = tk.transpose_back_project(tk.Volume(x, (1, 1, 1)), geom, True).data
+        want = oracle.back_cone_3d_T(x, geom.matrix_array(), 750.0, (10, 10), (1, 1, 1), True)
+        assert rel(got, want) < TOL
+
+    def test_paired_gradient_is_backprojection(self, tk):
+        geom = cone(tk, 16, 12, 1.6, 8)
+        x = torch.randn(16, 16, 16, device="cuda", requires_grad=True)
+        y = torch.randn(8, 12, 12, device="cuda")
+        (tk.ConeProjection3D.apply(x, geom) * y).sum().backward()
+        want = tk.back_project(tk.Sinogram(y, (1.6, 1.6)), geom).data
+        assert torch.equal(x.grad, want)
+
+    def test_matched_gradient_and_batch(self, tk):
+        geom = cone(tk, 16, 12, 1.6, 8)
+        x = torch.randn(3, 16, 16, 16, device="cuda", requires_grad=True)
+        y = torch.randn(3, 8, 12, 12, device="cuda")
+        (tk.ConeProjection3D.apply(x, geom, "matched") * y).sum().backward()
+        for i in range(3):
+            want = tk.transpose_forward_project(tk.Sinogram(y[i], (1.6, 1.6)), geom).data
+            assert rel(x.grad[i], want.cpu().numpy()) < 1e-5
+
+    def test_backprojection_layer_gradient(self, tk):
+        geom = cone(tk, 16, 12, 1.6, 8)
+        y = torch.randn(8, 12, 12, device="cuda", requires_grad=True)
+        x = torch.randn(16, 16, 16, device="cuda")
+        (tk.ConeBackProjection3D.apply(y, geom) * x).sum().backward()
+        assert torch.equal(y.grad, tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data)
+
+    def test_grad_check_projectors(self, tk):
+        ang = tk.circular_trajectory_2d(360, 2 * np.pi)
+        g = tk.GeometryParallel2D((32, 32), (1, 1), 64, 1.0, ang)
+        rep = tk.grad_check(tk.forward_projection_op(g), trials=3, epsilon=1.0)
+        assert rep.passed, str(rep)
+        rep = tk.grad_check(tk.forward_projection_op(g, matched=True), trials=3, epsilon=1.0, tolerance=1e-4)
+        assert rep.passed, str(rep)
+
+    def test_pyronn_listing1(self, tk):
+        params = dict(volume_shape=[32, 32, 32], volume_spacing=[0.5, 0.5, 0.5], detector_shape=[40, 60],
+                      detector_spacing=[1, 1], number_of_projections=36, angular_range=2 * np.pi,
+                      sdd=1200, sid=750)
+        geom = tk.GeometryCone3D(**params)
+        geom.set_trajectory(tk.circular_trajectory_3d(**params))
+        phantom = tk.phantoms.shepp_logan_3d(params["volume_shape"])[None]
+        sino = tk.ConeProjectionFor3D().forward(phantom, geom)
+        assert sino.shape == (1, 36, 40, 60)
+        x = tk.fft_and_ifft(sino, tk.shepp_logan_3D(**params))
+        reco = tk.ConeBackProjectionFor3D().forward(x, geom)
+        assert reco.shape == (1, 32, 32, 32) and torch.isfinite(reco).all()
+
+
+# ---------------------------------------------------------------------------
+# determinism, linearity, boundary
+# ---------------------------------------------------------------------------
+
+
+class TestProperties:
+    def test_repeat_runs_bit_identical(self, tk):
+        geom = cone(tk, 32, 40, 1.6, 12)
+        x = tk.Volume(np.random.default_rng(0).standard_normal((32,) * 3), (1, 1, 1))
+        a = tk.forward_project(x, geom).data
+        b = tk.forward_project(x, geom).data
+        assert torch.equal(a, b)
+        s = tk.Sinogram(a, (1.6, 1.6))
+        assert torch.equal(tk.back_project(s, geom, True).data, tk.back_project(s, geom, True).data)
+
+    def test_linearity(self, tk):
+        geom = cone(tk, 16, 16, 1.6, 8)
+        g = torch.Generator(device="cuda").manual_seed(0)
+        x, y = (torch.randn(16, 16, 16, device="cuda", generator=g) for _ in range(2))
+        step = 0.5
+        from paper_2511_08427_b200.projectors import bp_tensor, fp_tensor
+
+        lhs = fp_tensor(2.3 * x - 1.4 * y, geom, step)
+        rhs = 2.3 * fp_tensor(x, geom, step) - 1.4 * fp_tensor(y, geom, step)
+        assert float((lhs - rhs).abs().max()) <= 1e-5 * max(1.0, float(rhs.abs().max()))
+        s, t = (torch.randn(8, 16, 16, device="cuda", generator=g) for _ in range(2))
+        lhs = bp_tensor(2.3 * s - 1.4 * t, geom, True)
+        rhs = 2.3 * bp_tensor(s, geom, True) - 1.4 * bp_tensor(t, geom, True)
+        assert float((lhs - rhs).abs().max()) <= 1e-5 * max(1.0, float(rhs.abs().max()))
+
+    def test_boundary_numpy_roundtrip(self, tk):
+        from paper_2511_08427_b200 import ops
+
+        cfg = {"geometry_kind": "cone3d", "volume_shape": [16, 16, 16], "volume_spacing": [1, 1, 1],
+               "detector_shape": [12, 12], "detector_spacing": [1.6, 1.6], "number_of_projections": 8,
+               "angular_range": 2 * np.pi, "sdd": 1200.0, "sid": 750.0}
+        x = np.random.default_rng(7).standard_normal((16, 16, 16)).astype(np.float32)
+        a = ops.py_forward_project(x, cfg)
+        b = ops.py_forward_project(x, cfg)
+        assert isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+        assert a.shape == (8, 12, 12) and not np.shares_memory(a, b) and a.tobytes() == b.tobytes()
+        with pytest.raises(ops.BoundaryError, match="float32"):
+            ops.py_forward_project(x.astype(np.float64), cfg)
+        pinned = torch.from_numpy(x).pin_memory()
+        c = ops.py_forward_project(pinned, cfg)
+        assert isinstance(c, torch.Tensor) and not c.is_cuda and c.numpy().tobytes() == a.tobytes()
+        d = ops.py_forward_project(torch.from_numpy(x).cuda(), cfg)
+        assert d.is_cuda and d.cpu().numpy().tobytes() == a.tobytes()
+        assert ops.py_vjp_forward_project(a, cfg).tobytes() == ops.py_back_project(a, cfg).tobytes()
+
+    def test_concurrent_calls_match_serial(self, tk):
+        from concurrent.futures import ThreadPoolExecutor
+
+        from paper_2511_08427_b200 import ops
+
+        cfg = {"geometry_kind": "parallel2d", "volume_shape": [16, 16], "volume_spacing": [1, 1],
+               "detector_shape": [24], "detector_spacing": [1.0], "number_of_projections": 12,
+               "angular_range": 2 * np.pi}
+        rng = np.random.default_rng(3)
+        xs = [rng.standard_normal((16, 16)).astype(np.float32) for _ in range(8)]
+        serial = [ops.py_forward_project(x, cfg) for x in xs]
+        with ThreadPoolExecutor(max_workers=4) as pool:
+            par = list(pool.map(lambda x: ops.py_forward_project(x, cfg), xs))
+        assert all(s.tobytes() == p.tobytes() for s, p in zip(serial, par))
+
+    def test_fbp_disk_fidelity(self, tk):
+        shape, sp = (256, 256), (1.0, 1.0)
+        disk = tk.phantoms.disk_phantom(shape, 40.0, 1.0, sp)
+        geom = tk.GeometryParallel2D(shape, sp, 363, 1.0, tk.circular_trajectory_2d(360, 2 * np.pi))
+        rec = tk.fbp_parallel_2d(tk.forward_project(tk.Volume(disk, sp), geom), geom, "shepp_logan").data
+        y = torch.arange(256, device="cuda") - 127.5
+        mask = y[None, :] ** 2 + y[:, None] ** 2 <= (0.9 * 40.0) ** 2
+        rmse = float(torch.sqrt(torch.mean((rec[mask] - disk[mask]) ** 2)))
+        assert rmse < 0.05
+
+    def test_phantom_matches_oracle(self, tk, oracle):
+        got = tk.phantoms.shepp_logan_3d((64, 48, 32)).cpu().numpy()
+        want = oracle.shepp_logan_3d((64, 48, 32))
+        assert np.mean(got != want) < 1e-4
+
+    def test_native_library_was_used(self, tk):
+        from paper_2511_08427_b200 import _lib
+
+        before = _lib.launch_count()
+        geom = cone(tk, 16, 12, 1.6, 4)
+        tk.forward_project(tk.Volume(np.ones((16,) * 3), (1, 1, 1)), geom)
+        assert _lib.launch_count() > before
