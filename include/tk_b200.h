@@ -46,6 +46,11 @@ const char *tk_last_error(void);      /* thread-local; "" when no error */
 int tk_device_info(int *sm_major, int *sm_minor, int *sm_count);
 /* Number of kernel launches issued by this library since load (all threads). */
 unsigned long long tk_launch_count(void);
+/* The texture-gather kernels copy grids into pooled block-linear CUDA arrays
+ * that are kept between calls (stream-ordered reuse).  Bytes held / free all
+ * idle ones. */
+unsigned long long tk_cached_bytes(void);
+int tk_release_cached_memory(void);
 
 /* ---- parallel-beam 2D ------------------------------------------------------
  * replaces _kernels.forward_parallel_2d (_kernels.py:160-171), called from

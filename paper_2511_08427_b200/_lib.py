@@ -30,6 +30,8 @@ SIGNATURES = {
     "tk_last_error": [],
     "tk_device_info": [ctypes.POINTER(_c_int)] * 3,
     "tk_launch_count": [],
+    "tk_cached_bytes": [],
+    "tk_release_cached_memory": [],
     "tk_forward_parallel_2d": [_ptr, _c_int, _c_int, _c_dbl, _c_dbl, _dptr, _dptr, _c_int, _c_int,
                                _c_dbl, _c_dbl, _ptr, _ptr],
     "tk_back_parallel_2d": [_ptr, _c_int, _c_int, _dptr, _dptr, _c_dbl, _c_int, _c_int, _c_dbl,
@@ -85,7 +87,7 @@ def load(path: Path | str | None = None):
             fn.argtypes = args
             if name == "tk_last_error":
                 fn.restype = ctypes.c_char_p
-            elif name == "tk_launch_count":
+            elif name in ("tk_launch_count", "tk_cached_bytes"):
                 fn.restype = ctypes.c_ulonglong
             else:
                 fn.restype = _c_int

@@ -17,9 +17,12 @@
 //     along z; only the row coordinate advances.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "tk_common.cuh"
+#include "tk_tex.cuh"
 
 namespace tk {
 
@@ -186,6 +189,89 @@ __global__ void __launch_bounds__(kFpBX *kFpBY)
   *dst = acc * (float)step;
 }
 
+// Texture-gather variant: the volume lives in a layered CUDA array (layer =
+// z slice, block-linear (x, y) tiles), each sample fetches its two 2x2 tap
+// quads with TLD4 (exact fp32 texels; the interpolation weights stay fp32 in
+// registers).  x/y zero-extension comes from border addressing; only the
+// layer index needs an explicit range check (layers clamp).
+__device__ __forceinline__ float trilinear_tex(cudaTextureObject_t tex, int nz, float fx, float fy,
+                                               float fz) {
+  const float flx = floorf(fx), fly = floorf(fy), flz = floorf(fz);
+  const float wx = fx - flx, wy = fy - fly, wz = fz - flz;
+  const int lz = (int)flz - 1;  // unpadded index of the lower slice
+  float lo = 0.f, hi = 0.f;
+  // gather centre (flx, fly) in unpadded texel units = (ix_u + 1, iy_u + 1)
+  if ((unsigned)lz < (unsigned)nz) {
+    const float4 g = gather_a2d(tex, lz, flx, fly);
+    lo = lerpf(lerpf(g.w, g.z, wx), lerpf(g.x, g.y, wx), wy);
+  }
+  if ((unsigned)(lz + 1) < (unsigned)nz) {
+    const float4 g = gather_a2d(tex, lz + 1, flx, fly);
+    hi = lerpf(lerpf(g.w, g.z, wx), lerpf(g.x, g.y, wx), wy);
+  }
+  return lerpf(lo, hi, wz);
+}
+
+__global__ void __launch_bounds__(kFpBX *kFpBY)
+    cone_fp_tex_kernel(cudaTextureObject_t tex, int nx, int ny, int nz, double sx, double sy,
+                       double sz, const ConeRayView *__restrict__ views, int rows, int cols,
+                       double step, float *__restrict__ out) {
+  const int c = blockIdx.x * kFpBX + threadIdx.x;
+  const int r = blockIdx.y * kFpBY + threadIdx.y;
+  const int v = blockIdx.z;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const ConeRayView V = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(V, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  float acc = 0.f;
+  const int nfull = rs.n - 1;
+#pragma unroll 4
+  for (int k = 0; k < nfull; ++k) {
+    const float kf = (float)k + 0.5f;
+    acc += trilinear_tex(tex, nz, fmaf(kf, rs.gx, rs.ex), fmaf(kf, rs.gy, rs.ey),
+                         fmaf(kf, rs.gz, rs.ez));
+  }
+  const float kf = (float)nfull + 0.5f * rs.last;
+  acc += rs.last * trilinear_tex(tex, nz, fmaf(kf, rs.gx, rs.ex), fmaf(kf, rs.gy, rs.ey),
+                                 fmaf(kf, rs.gz, rs.ez));
+  *dst = acc * (float)step;
+}
+
+// Hardware-trilinear variant (benchmark comparison only: the texture unit's
+// 8-bit fractional weights cost accuracy).  3D array, border 0.
+__global__ void __launch_bounds__(kFpBX *kFpBY)
+    cone_fp_hwtex_kernel(cudaTextureObject_t tex, int nx, int ny, int nz, double sx, double sy,
+                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
+                         double step, float *__restrict__ out) {
+  const int c = blockIdx.x * kFpBX + threadIdx.x;
+  const int r = blockIdx.y * kFpBY + threadIdx.y;
+  const int v = blockIdx.z;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const ConeRayView V = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(V, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  // padded index p -> unpadded texel coordinate p - 1 + 0.5
+  const float ex = rs.ex - 0.5f, ey = rs.ey - 0.5f, ez = rs.ez - 0.5f;
+  float acc = 0.f;
+  const int nfull = rs.n - 1;
+#pragma unroll 4
+  for (int k = 0; k < nfull; ++k) {
+    const float kf = (float)k + 0.5f;
+    acc += tex3D<float>(tex, fmaf(kf, rs.gx, ex), fmaf(kf, rs.gy, ey), fmaf(kf, rs.gz, ez));
+  }
+  const float kf = (float)nfull + 0.5f * rs.last;
+  acc += rs.last * tex3D<float>(tex, fmaf(kf, rs.gx, ex), fmaf(kf, rs.gy, ey), fmaf(kf, rs.gz, ez));
+  *dst = acc * (float)step;
+}
+
 // Exact transpose of cone_fp_kernel: scatter y * seg * weights into the padded
 // accumulation volume (fp32 atomics).
 __device__ __forceinline__ void trilinear_scatter(float *__restrict__ adjp, int nxp, int nyp,
@@ -257,6 +343,7 @@ struct BpParams {
   float cx, cy, cz;  // volume centre (index units)
   int accumulate;
   float *out;
+  cudaTextureObject_t tex;  // layered sinogram (texture variants only)
 };
 
 // Column taps (clamped indices + weights, zero outside [0, cols)).
@@ -372,6 +459,110 @@ __global__ void __launch_bounds__(kBpBX *kBpBY) cone_bp_kernel(const BpParams p)
   }
 }
 
+// Texture-gather variant: the (band) sinogram lives in a layered CUDA array
+// (layer = view); each update fetches its 2x2 tap quad with one TLD4, the
+// zero outside the detector comes from border addressing, and the bilinear
+// weights stay exact fp32.  HW = true uses the texture unit's own bilinear
+// filter instead (8-bit weights; benchmark comparison only).
+template <int ZB, bool ZINV, bool WEIGHTED, bool HW>
+__global__ void __launch_bounds__(kBpBX *kBpBY) cone_bp_tex_kernel(const BpParams p) {
+  __shared__ ConeVoxView sv[kBpChunk];
+  const int ix = blockIdx.x * kBpBX + threadIdx.x;
+  const int iy = blockIdx.y * kBpBY + threadIdx.y;
+  const int zl0 = blockIdx.z * ZB;
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx;
+  const float yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  const int tid = threadIdx.y * kBpBX + threadIdx.x;
+  const float colmax = (float)(p.cols - 1);
+
+  float acc[ZB];
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) acc[k] = 0.f;
+
+  for (int v0 = 0; v0 < p.n_views; v0 += kBpChunk) {
+    const int nch = min(kBpChunk, p.n_views - v0);
+    __syncthreads();
+    for (int i = tid; i < nch * 12; i += kBpBX * kBpBY)
+      reinterpret_cast<float *>(sv)[i] = __ldg(reinterpret_cast<const float *>(p.views + v0) + i);
+    __syncthreads();
+    if (!active) continue;
+    for (int j = 0; j < nch; ++j) {
+      const ConeVoxView &V = sv[j];
+      const int layer = v0 + j;
+      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+      if (ZINV) {
+        if (!(w0 > (float)kTiny)) continue;
+        const float rw = 1.f / w0;
+        const float fc = fmaf(a0, rw, p.cu);
+        const float flc = floorf(fc);
+        if (!(flc >= -1.f && flc <= colmax)) continue;  // both column taps off the detector
+        const float wc = fc - flc;
+        float q = 1.f;
+        if (WEIGHTED) {
+          q = p.sid * rw;
+          q *= q;
+        }
+        const float g0 = q * (1.f - wc), g1 = q * wc;
+        const float fr0 = fmaf(b0, rw, p.cv);
+        const float dr = V.b[2] * rw;
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          if (HW) {
+            acc[k] = fmaf(q, tex2DLayered<float>(p.tex, fc + 0.5f, fr + 0.5f, layer), acc[k]);
+          } else {
+            const float flr = floorf(fr);
+            const float wr = fr - flr;
+            const float4 t = gather_a2d(p.tex, layer, flc + 1.f, flr + 1.f);
+            const float top = fmaf(g1, t.z, g0 * t.w);  // detector row r0: (c0, c0 + 1)
+            const float bot = fmaf(g1, t.y, g0 * t.x);  // detector row r0 + 1
+            acc[k] += fmaf(wr, bot - top, top);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float kf = (float)k;
+          const float w = fmaf(kf, V.w[2], w0);
+          if (!(w > (float)kTiny)) continue;
+          const float rw = 1.f / w;
+          const float fc = fmaf(fmaf(kf, V.a[2], a0), rw, p.cu);
+          const float fr = fmaf(fmaf(kf, V.b[2], b0), rw, p.cv);
+          float q = 1.f;
+          if (WEIGHTED) {
+            q = p.sid * rw;
+            q *= q;
+          }
+          float val;
+          if (HW) {
+            val = tex2DLayered<float>(p.tex, fc + 0.5f, fr + 0.5f, layer);
+          } else {
+            const float flc = floorf(fc), flr = floorf(fr);
+            const float wc = fc - flc, wr = fr - flr;
+            const float4 t = gather_a2d(p.tex, layer, flc + 1.f, flr + 1.f);
+            const float top = lerpf(t.w, t.z, wc), bot = lerpf(t.x, t.y, wc);
+            val = lerpf(top, bot, wr);
+          }
+          acc[k] = fmaf(q, val, acc[k]);
+        }
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
 // Exact transpose of the (unweighted or weighted) voxel-driven back projector:
 // splat each voxel into the detector with the same bilinear weights.
 __global__ void __launch_bounds__(256)
@@ -438,6 +629,16 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
+// Forward-projector algorithm: TK_FP_ALGO = tex (default) | ldg | hwtex.
+enum class FpAlgo { kTex, kLdg, kHwTex };
+
+static FpAlgo fp_algo() {
+  const char *e = getenv("TK_FP_ALGO");
+  if (e && !strcmp(e, "ldg")) return FpAlgo::kLdg;
+  if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
+  return FpAlgo::kTex;
+}
+
 static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double sy,
                      double sx, const double *sources, const double *minv, int n_views,
                      int rows, int cols, double step, float *out, cudaStream_t st,
@@ -449,11 +650,27 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   }
   Scratch dviews, volp;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
+  dim3 block(kFpBX, kFpBY);
+  dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
+  const FpAlgo algo = fp_algo();
+  if (!adjoint && algo != FpAlgo::kLdg) {
+    TexLease lease;
+    const bool hw = algo == FpAlgo::kHwTex;
+    TK_TRY_CUDA(tex_acquire(vol, nx, ny, nz, hw ? TexKind::kVolumeLinear : TexKind::kLayeredPoint,
+                            st, lease));
+    if (hw)
+      cone_fp_hwtex_kernel<<<grid, block, 0, st>>>(lease.tex, nx, ny, nz, sx, sy, sz,
+                                                   dviews.as<ConeRayView>(), rows, cols, step, out);
+    else
+      cone_fp_tex_kernel<<<grid, block, 0, st>>>(lease.tex, nx, ny, nz, sx, sy, sz,
+                                                 dviews.as<ConeRayView>(), rows, cols, step, out);
+    tex_release(lease, st);
+    TK_LAUNCHED(hw ? "cone_fp_hwtex_kernel" : "cone_fp_tex_kernel");
+    return TK_OK;
+  }
   const long long npad = (long long)(nz + 2) * (ny + 2) * (nx + 2);
   TK_TRY_CUDA(volp.alloc(sizeof(float) * npad, st));
   const unsigned pgrid = (unsigned)std::min<long long>(ceil_div(npad, 256), 148LL * 32);
-  dim3 block(kFpBX, kFpBY);
-  dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   if (!adjoint) {
     pad3d_kernel<<<pgrid, 256, 0, st>>>(vol, nz, ny, nx, volp.as<float>());
     TK_LAUNCHED("pad3d_kernel");
@@ -475,13 +692,34 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   return TK_OK;
 }
 
+// Back-projector algorithm: TK_BP_ALGO = ldg (default) | tex | hwtex.
+enum class BpAlgo { kLdg, kTex, kHwTex };
+
+static BpAlgo bp_algo() {
+  const char *e = getenv("TK_BP_ALGO");
+  if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
+  if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
+  return BpAlgo::kLdg;
+}
+
 template <int ZB, bool ZINV>
-static void launch_bp_t(const BpParams &p, bool weighted, dim3 grid, dim3 block,
+static void launch_bp_t(const BpParams &p, bool weighted, BpAlgo algo, dim3 grid, dim3 block,
                         cudaStream_t st) {
-  if (weighted)
+  if (algo == BpAlgo::kTex) {
+    if (weighted)
+      cone_bp_tex_kernel<ZB, ZINV, true, false><<<grid, block, 0, st>>>(p);
+    else
+      cone_bp_tex_kernel<ZB, ZINV, false, false><<<grid, block, 0, st>>>(p);
+  } else if (algo == BpAlgo::kHwTex) {
+    if (weighted)
+      cone_bp_tex_kernel<ZB, ZINV, true, true><<<grid, block, 0, st>>>(p);
+    else
+      cone_bp_tex_kernel<ZB, ZINV, false, true><<<grid, block, 0, st>>>(p);
+  } else if (weighted) {
     cone_bp_kernel<ZB, ZINV, true><<<grid, block, 0, st>>>(p);
-  else
+  } else {
     cone_bp_kernel<ZB, ZINV, false><<<grid, block, 0, st>>>(p);
+  }
 }
 
 }  // namespace tk
@@ -559,10 +797,20 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   constexpr int ZB = 8;
   dim3 block(kBpBX, kBpBY);
   dim3 grid(ceil_div(nx, kBpBX), ceil_div(ny, kBpBY), ceil_div(z_count, ZB));
+  const BpAlgo algo = n_views <= 2048 ? bp_algo() : BpAlgo::kLdg;  // layered arrays: <= 2048 layers
+  TexLease lease;
+  p.tex = 0;
+  if (algo != BpAlgo::kLdg) {
+    TK_TRY_CUDA(tex_acquire(sino, cols, band_rows, n_views,
+                            algo == BpAlgo::kHwTex ? TexKind::kLayeredLinear : TexKind::kLayeredPoint,
+                            st, lease));
+    p.tex = lease.tex;
+  }
   if (zinv)
-    launch_bp_t<ZB, true>(p, weighted != 0, grid, block, st);
+    launch_bp_t<ZB, true>(p, weighted != 0, algo, grid, block, st);
   else
-    launch_bp_t<ZB, false>(p, weighted != 0, grid, block, st);
+    launch_bp_t<ZB, false>(p, weighted != 0, algo, grid, block, st);
+  if (lease.slot) tex_release(lease, st);
   TK_LAUNCHED("cone_bp_kernel");
   return TK_OK;
 }

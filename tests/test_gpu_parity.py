@@ -361,7 +361,7 @@ class TestProperties:
     def test_phantom_matches_oracle(self, tk, oracle):
         got = tk.phantoms.shepp_logan_3d((64, 48, 32)).cpu().numpy()
         want = oracle.shepp_logan_3d((64, 48, 32))
-        assert np.mean(got != want) < 1e-4
+        assert np.mean(np.abs(got - want) > 1e-6) < 1e-4  # fp32 vs fp64 values
 
     def test_native_library_was_used(self, tk):
         from paper_2511_08427_b200 import _lib
