@@ -189,6 +189,137 @@ __global__ void __launch_bounds__(kFpBX *kFpBY)
   *dst = acc * (float)step;
 }
 
+// ---------------------------------------------------------------------------
+// Forward projection, orientation-matched LDG variant ("ldg2", default).
+//
+// * The volume is kept with a TWO-voxel zero margin in two orientations: x
+//   fastest (A) and y fastest (B, x/y exchanged).  Each view uses the copy
+//   whose fastest axis is most aligned with the detector u direction, and a
+//   warp covers 32 consecutive detector columns, so the 32 rays' samples at a
+//   step lie along the fast axis and each tap load touches one or two lines.
+// * With the 2-voxel margin every cell a sample can reach (inside the clip
+//   box up to float32 rounding) is addressable and its out-of-volume taps read
+//   zero, which IS the reference's zero-extended interpolant -- no per-sample
+//   range test, no clamping.
+// * A thread keeps the taps of its current cell (and their differences along
+//   the fast axis) in registers; a sample that stays in the same cell (about
+//   half of them at step = s/2) issues no load.
+// ---------------------------------------------------------------------------
+constexpr int kFp2BX = 32, kFp2BY = 4;
+constexpr int kFpMargin = 2;
+
+// vol (nz, ny, nx) -> copy with a kFpMargin zero margin; swap_xy selects the
+// y-fastest orientation out[z][x][y].  Tiled through shared memory so both
+// the read and the (possibly transposed) write are coalesced.
+__global__ void pad_margin_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
+                                  float *__restrict__ out) {
+  __shared__ float tile[32][33];
+  constexpr int m = kFpMargin;
+  const int nxp = nx + 2 * m, nyp = ny + 2 * m;
+  const int z = blockIdx.z;  // padded z
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const bool zin = z >= m && z < nz + m;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int y = y0 + j, x = x0 + threadIdx.x;  // padded coordinates
+    float v = 0.f;
+    if (zin && y >= m && y < ny + m && x >= m && x < nx + m)
+      v = __ldg(vol + ((long long)(z - m) * ny + (y - m)) * nx + (x - m));
+    tile[j][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    if (swap_xy) {
+      const int x = x0 + j, y = y0 + threadIdx.x;
+      if (x < nxp && y < nyp) out[((long long)z * nxp + x) * nyp + y] = tile[threadIdx.x][j];
+    } else {
+      const int y = y0 + j, x = x0 + threadIdx.x;
+      if (x < nxp && y < nyp) out[((long long)z * nyp + y) * nxp + x] = tile[j][threadIdx.x];
+    }
+  }
+}
+
+struct Fp2View {
+  ConeRayView ray;
+  int swap;  // 1: use the y-fastest copy (x and y exchanged)
+  int pad;
+};
+
+struct CellTaps {  // the 8 taps of one cell: v[z][b][a], with d = v[..][1] - v[..][0]
+  float v00, d00, v01, d01, v10, d10, v11, d11;
+};
+
+__device__ __forceinline__ void load_cell(const float *__restrict__ p, int pa, int ps, CellTaps &t) {
+  const float a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + pa), d = __ldg(p + pa + 1);
+  const float e = __ldg(p + ps), f = __ldg(p + ps + 1), g = __ldg(p + ps + pa),
+              h = __ldg(p + ps + pa + 1);
+  t.v00 = a;
+  t.d00 = b - a;
+  t.v01 = c;
+  t.d01 = d - c;
+  t.v10 = e;
+  t.d10 = f - e;
+  t.v11 = g;
+  t.d11 = h - g;
+}
+
+__device__ __forceinline__ float interp_cell(const CellTaps &t, float wa, float wb, float wz) {
+  const float a0 = fmaf(wa, t.d00, t.v00), a1 = fmaf(wa, t.d01, t.v01);
+  const float b0 = fmaf(wa, t.d10, t.v10), b1 = fmaf(wa, t.d11, t.v11);
+  const float lo = fmaf(wb, a1 - a0, a0), hi = fmaf(wb, b1 - b0, b0);
+  return fmaf(wz, hi - lo, lo);
+}
+
+__global__ void __launch_bounds__(kFp2BX *kFp2BY)
+    cone_fp2_kernel(const float *__restrict__ volA, const float *__restrict__ volB, int nx, int ny,
+                    int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
+                    int rows, int cols, double step, float *__restrict__ out) {
+  const int c = blockIdx.x * kFp2BX + threadIdx.x;
+  const int r = blockIdx.y * kFp2BY + threadIdx.y;
+  const int v = blockIdx.z;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  // fast axis "a", middle axis "b": (x, y) for copy A, (y, x) for copy B.
+  // rs.e* are one-voxel-padded coordinates; the copies carry a 2-voxel margin.
+  const float *vol = W.swap ? volB : volA;
+  const int na = W.swap ? ny : nx, nb = W.swap ? nx : ny;
+  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const int pa = na + 2 * kFpMargin;        // padded row pitch
+  const int ps = (nb + 2 * kFpMargin) * pa;  // padded slice pitch
+  int cell = -1;
+  CellTaps t = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float acc = 0.f;
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k, kf += 1.f) {
+    const float fa = fmaf(kf, ga, ea), fb = fmaf(kf, gb, eb), fz = fmaf(kf, gz, ez);
+    const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
+    const int id = (int)lz * ps + (int)lb * pa + (int)la;
+    if (id != cell) {
+      cell = id;
+      load_cell(vol + id, pa, ps, t);
+    }
+    acc += interp_cell(t, fa - la, fb - lb, fz - lz);
+  }
+  {  // last (possibly partial) segment: midpoint at t + seg/2, weight seg/step
+    kf = (float)nfull + 0.5f * rs.last;
+    const float fa = fmaf(kf, ga, ea), fb = fmaf(kf, gb, eb), fz = fmaf(kf, gz, ez);
+    const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
+    const int id = (int)lz * ps + (int)lb * pa + (int)la;
+    if (id != cell) load_cell(vol + id, pa, ps, t);
+    acc = fmaf(rs.last, interp_cell(t, fa - la, fb - lb, fz - lz), acc);
+  }
+  *dst = acc * (float)step;
+}
+
 // Texture-gather variant: the volume lives in a layered CUDA array (layer =
 // z slice, block-linear (x, y) tiles), each sample fetches its two 2x2 tap
 // quads with TLD4 (exact fp32 texels; the interpolation weights stay fp32 in
@@ -629,14 +760,52 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = tex (default) | ldg | hwtex.
-enum class FpAlgo { kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg2 (default) | ldg | tex | hwtex.
+enum class FpAlgo { kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
   if (e && !strcmp(e, "ldg")) return FpAlgo::kLdg;
+  if (e && !strcmp(e, "tex")) return FpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
-  return FpAlgo::kTex;
+  return FpAlgo::kLdg2;
+}
+
+static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                      const double *sources, const double *minv, int n_views, int rows, int cols,
+                      double step, float *out, cudaStream_t st) {
+  std::vector<Fp2View> hv(n_views);
+  bool need_a = false, need_b = false;
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
+    // detector u direction (column 0 of M^-1) in voxel units
+    const double ux = fabs(minv[9 * i + 0] / sx), uy = fabs(minv[9 * i + 3] / sy);
+    hv[i].swap = uy > ux ? 1 : 0;
+    hv[i].pad = 0;
+    (hv[i].swap ? need_b : need_a) = true;
+  }
+  Scratch dviews, volA, volB;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
+  constexpr int m2 = 2 * kFpMargin;
+  const long long npad = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  dim3 tg(ceil_div(nx + m2, 32), ceil_div(ny + m2, 32), nz + m2);
+  if (need_a) {
+    TK_TRY_CUDA(volA.alloc(sizeof(float) * npad, st));
+    pad_margin_kernel<<<tg, dim3(32, 8), 0, st>>>(vol, nz, ny, nx, 0, volA.as<float>());
+    TK_LAUNCHED("pad_margin_kernel");
+  }
+  if (need_b) {
+    TK_TRY_CUDA(volB.alloc(sizeof(float) * npad, st));
+    pad_margin_kernel<<<tg, dim3(32, 8), 0, st>>>(vol, nz, ny, nx, 1, volB.as<float>());
+    TK_LAUNCHED("pad_margin_kernel");
+  }
+  dim3 block(kFp2BX, kFp2BY);
+  dim3 grid(ceil_div(cols, kFp2BX), ceil_div(rows, kFp2BY), n_views);
+  cone_fp2_kernel<<<grid, block, 0, st>>>(volA.as<float>(), volB.as<float>(), nx, ny, nz, sx, sy, sz,
+                                          dviews.as<Fp2View>(), rows, cols, step, out);
+  TK_LAUNCHED("cone_fp2_kernel");
+  return TK_OK;
 }
 
 static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double sy,
@@ -653,6 +822,8 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
+  if (!adjoint && algo == FpAlgo::kLdg2)
+    return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo != FpAlgo::kLdg) {
     TexLease lease;
     const bool hw = algo == FpAlgo::kHwTex;

@@ -7,10 +7,14 @@
 // real rows a, b are filtered with ONE complex transform of z = a + i b:
 // IFFT(W * FFT(z)) = filt(a) + i filt(b).
 //
-// One CTA owns a row pair at a time (grid-stride); the n_pad-point transform
-// runs in shared memory (radix-2, decimation in time forward on bit-reversed
-// input, decimation in frequency inverse producing bit-reversed output, so no
-// explicit permutation pass is needed).
+// One CTA owns a row pair at a time (grid-stride).  The n_pad-point transform
+// is a mixed-radix Stockham FFT (radix 8 stages, one radix 4/2 stage) with
+// every butterfly in registers and shared memory only between stages, so a
+// 2048-point transform is 4 stages instead of 11.  The first forward stage
+// reads the (pre-weighted, zero-padded) rows straight from global memory and
+// the last inverse stage writes the cropped result straight back; the weights
+// and the 1/n_pad normalisation are applied while loading the first inverse
+// stage.  The inverse uses IFFT(y) = conj(FFT(conj(y))) / n.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -25,13 +29,52 @@ struct FilterParams {
   const float *in;
   float *out;
   long long n_rows;
-  int width, band_rows, row_offset, det_rows, n_pad, log2n;
-  const float2 *tw;    // exp(-2 pi i k / n_pad), k < n_pad/2
-  const float *wgt;    // half weights * scale / n_pad, n_pad/2 + 1 entries
-  float sdd, du, dv;   // obliquity pre-weight (disabled when sdd <= 0)
+  int width, band_rows, row_offset, det_rows, n_pad;
+  const float2 *tw;  // exp(-2 pi i m / n_pad), m < n_pad
+  const float *wgt;   // half weights * scale / n_pad, n_pad/2 + 1 entries
+  float sdd, du, dv;  // obliquity pre-weight (disabled when sdd <= 0)
 };
 
-__device__ __forceinline__ unsigned bitrev(unsigned i, int bits) { return __brev(i) >> (32 - bits); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // * (-i)
+
+// forward DFTs in registers, natural order
+__device__ __forceinline__ void dft2(float2 *v) {
+  const float2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+__device__ __forceinline__ void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+  const float2 s02 = cadd(x0, x2), d02 = csub(x0, x2), s13 = cadd(x1, x3), d13 = csub(x1, x3);
+  x0 = cadd(s02, s13);
+  x2 = csub(s02, s13);
+  x1 = cadd(d02, mul_mi(d13));
+  x3 = csub(d02, mul_mi(d13));
+}
+
+__device__ __forceinline__ void dft8(float2 *v) {
+  float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4(e0, e1, e2, e3);
+  dft4(o0, o1, o2, o3);
+  const float r = 0.70710678118654752440f;
+  o1 = make_float2(r * (o1.x + o1.y), r * (o1.y - o1.x));    // * W8^1 = (1 - i)/sqrt2
+  o2 = mul_mi(o2);                                           // * W8^2 = -i
+  o3 = make_float2(r * (o3.y - o3.x), -r * (o3.x + o3.y));   // * W8^3 = (-1 - i)/sqrt2
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1);
+  v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2);
+  v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3);
+  v[7] = csub(e3, o3);
+}
 
 __device__ __forceinline__ float preweight(const FilterParams &p, long long row, int i) {
   if (!(p.sdd > 0.f)) return 1.f;
@@ -41,76 +84,149 @@ __device__ __forceinline__ float preweight(const FilterParams &p, long long row,
   return p.sdd / sqrtf(fmaf(p.sdd, p.sdd, fmaf(u, u, v * v)));
 }
 
-__global__ void __launch_bounds__(256) fft_filter_kernel(const FilterParams p) {
+// Source of stage inputs: 0 = shared buffer, 1 = global rows (first forward
+// stage), 2 = shared buffer x weights, conjugated (first inverse stage).
+// Destination: 0 = shared buffer, 1 = global rows conjugated (last inverse stage).
+template <int R>
+__device__ __forceinline__ void stockham_stage(float2 *x, const float2 *tw, int N, int Ns, int src,
+                                               int dst, const FilterParams &p, const float *ia,
+                                               const float *ib, long long ra, long long rb,
+                                               bool has_b, float *oa, float *ob, const float *wgt) {
+  const int nb = N / R;
+  const int tstride = N / (Ns * R);
+  float2 v[8];
+  // butterflies of this thread: blockDim >= N/8, so at most 8/R of them
+  constexpr int kMaxB = 8 / R;
+  int jj[kMaxB];
+  float2 vv[kMaxB][R];
+  int cnt = 0;
+#pragma unroll
+  for (int c = 0; c < kMaxB; ++c) {
+    const int j = threadIdx.x + c * blockDim.x;
+    if (j >= nb) break;
+    ++cnt;
+    jj[c] = j;
+    const int k = j % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = j + r * nb;
+      float2 z;
+      if (src == 1) {
+        float a = 0.f, b = 0.f;
+        if (e < p.width) {
+          a = __ldg(ia + e) * preweight(p, ra, e);
+          if (has_b) b = __ldg(ib + e) * preweight(p, rb, e);
+        }
+        z = make_float2(a, b);
+      } else {
+        z = x[e];
+        if (src == 2) {
+          const float w = wgt[e <= N / 2 ? e : N - e];
+          z = make_float2(z.x * w, -z.y * w);
+        }
+      }
+      v[r] = (r > 0 && Ns > 1) ? cmul(z, tw[r * k * tstride]) : z;
+    }
+    if (R == 8) dft8(v);
+    if (R == 4) dft4(v[0], v[1], v[2], v[3]);
+    if (R == 2) dft2(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) vv[c][r] = v[r];
+  }
+  __syncthreads();  // every thread has read its inputs (in-place buffer)
+#pragma unroll
+  for (int c = 0; c < kMaxB; ++c) {
+    if (c >= cnt) break;
+    const int j = jj[c];
+    const int k = j % Ns;
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int o = base + r * Ns;
+      if (dst == 1) {
+        if (o < p.width) {
+          oa[o] = vv[c][r].x;
+          if (has_b) ob[o] = -vv[c][r].y;
+        }
+      } else {
+        x[o] = vv[c][r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Compile-time stage plan for N = 2^LOGN: radix-8 stages first, then one
+// radix-4 or radix-2 stage; stage S of the forward (INV = false) or inverse
+// pass, recursing to the next stage.
+template <int LOGN>
+struct FftPlan {
+  static constexpr int kN = 1 << LOGN;
+  static constexpr int kStages8 = LOGN / 3;
+  static constexpr int kRem = LOGN % 3;
+  static constexpr int kStages = kStages8 + (kRem ? 1 : 0);
+  static constexpr int radix(int s) { return s < kStages8 ? 8 : (kRem == 1 ? 2 : 4); }
+  static constexpr int span(int s) { return s == 0 ? 1 : span(s - 1) * radix(s - 1); }
+};
+
+template <int LOGN, bool INV, int S>
+__device__ __forceinline__ void fft_pass(float2 *x, const float2 *tw, const FilterParams &p,
+                                         const float *ia, const float *ib, long long ra,
+                                         long long rb, bool has_b, float *oa, float *ob,
+                                         const float *wgt) {
+  using P = FftPlan<LOGN>;
+  if constexpr (S < P::kStages) {
+    constexpr int src = S == 0 ? (INV ? 2 : 1) : 0;
+    constexpr int dst = (INV && S == P::kStages - 1) ? 1 : 0;
+    stockham_stage<P::radix(S)>(x, tw, P::kN, P::span(S), src, dst, p, ia, ib, ra, rb, has_b, oa,
+                                ob, wgt);
+    fft_pass<LOGN, INV, S + 1>(x, tw, p, ia, ib, ra, rb, has_b, oa, ob, wgt);
+  }
+}
+
+template <int LOGN>
+constexpr int filter_threads() {
+  return (1 << LOGN) / 8 < 32 ? 32 : ((1 << LOGN) / 8 > 1024 ? 1024 : (1 << LOGN) / 8);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(filter_threads<LOGN>()) fft_filter_kernel(const FilterParams p) {
   extern __shared__ float smem[];
-  const int N = p.n_pad;
+  constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);
   float2 *tw = x + N;
-  float *wgt = reinterpret_cast<float *>(tw + N / 2);
-  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) tw[i] = p.tw[i];
+  float *wgt = reinterpret_cast<float *>(tw + N);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = p.tw[i];
   for (int i = threadIdx.x; i <= N / 2; i += blockDim.x) wgt[i] = p.wgt[i];
+  __syncthreads();
   const long long n_pairs = (p.n_rows + 1) / 2;
   for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
     const long long ra = 2 * pair, rb = ra + 1;
     const bool has_b = rb < p.n_rows;
     const float *ia = p.in + ra * p.width;
     const float *ib = p.in + rb * p.width;
-    __syncthreads();  // previous pair's output reads complete before overwrite
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      float a = 0.f, b = 0.f;
-      if (i < p.width) {
-        a = __ldg(ia + i) * preweight(p, ra, i);
-        if (has_b) b = __ldg(ib + i) * preweight(p, rb, i);
-      }
-      x[bitrev(i, p.log2n)] = make_float2(a, b);
-    }
-    // forward DIT
-    for (int s = 1; s <= p.log2n; ++s) {
-      __syncthreads();
-      const int half = 1 << (s - 1);
-      const int tstride = N >> s;
-      for (int bI = threadIdx.x; bI < N / 2; bI += blockDim.x) {
-        const int pos = bI & (half - 1);
-        const int i0 = ((bI >> (s - 1)) << s) + pos;
-        const int i1 = i0 + half;
-        const float2 w = tw[pos * tstride];
-        const float2 u = x[i0], v = x[i1];
-        const float2 t = make_float2(w.x * v.x - w.y * v.y, w.x * v.y + w.y * v.x);
-        x[i0] = make_float2(u.x + t.x, u.y + t.y);
-        x[i1] = make_float2(u.x - t.x, u.y - t.y);
-      }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
-      const float w = wgt[k <= N / 2 ? k : N - k];
-      const float2 v = x[k];
-      x[k] = make_float2(v.x * w, v.y * w);
-    }
-    // inverse DIF with conjugate twiddles -> bit-reversed output
-    for (int s = p.log2n; s >= 1; --s) {
-      __syncthreads();
-      const int half = 1 << (s - 1);
-      const int tstride = N >> s;
-      for (int bI = threadIdx.x; bI < N / 2; bI += blockDim.x) {
-        const int pos = bI & (half - 1);
-        const int i0 = ((bI >> (s - 1)) << s) + pos;
-        const int i1 = i0 + half;
-        const float2 w = tw[pos * tstride];
-        const float2 u = x[i0], v = x[i1];
-        const float2 d = make_float2(u.x - v.x, u.y - v.y);
-        x[i0] = make_float2(u.x + v.x, u.y + v.y);
-        x[i1] = make_float2(w.x * d.x + w.y * d.y, w.x * d.y - w.y * d.x);
-      }
-    }
-    __syncthreads();
     float *oa = p.out + ra * p.width;
     float *ob = p.out + rb * p.width;
-    for (int i = threadIdx.x; i < p.width; i += blockDim.x) {
-      const float2 v = x[bitrev(i, p.log2n)];
-      oa[i] = v.x;
-      if (has_b) ob[i] = v.y;
-    }
+    fft_pass<LOGN, false, 0>(x, tw, p, ia, ib, ra, rb, has_b, oa, ob, wgt);  // forward
+    fft_pass<LOGN, true, 0>(x, tw, p, ia, ib, ra, rb, has_b, oa, ob, wgt);   // x W, inverse
   }
+}
+
+template <int LOGN>
+static cudaError_t launch_filter(const FilterParams &p, size_t smem, cudaStream_t st) {
+  constexpr int N = 1 << LOGN;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fft_filter_kernel<LOGN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  // blockDim >= N/8 keeps every stage at <= 8/R butterflies per thread
+  const int threads = filter_threads<LOGN>();
+  const long long pairs = (p.n_rows + 1) / 2;
+  const int per_sm = std::max(1, std::min<int>((int)((200 * 1024) / smem), 2048 / threads));
+  const unsigned grid = (unsigned)std::min<long long>(pairs, (long long)sm_count() * per_sm);
+  fft_filter_kernel<LOGN><<<grid, threads, smem, st>>>(p);
+  return cudaGetLastError();
 }
 
 }  // namespace tk
@@ -126,20 +242,19 @@ extern "C" int tk_fft_filter_rows_ex(const float *in, long long n_rows, int widt
   if (n_rows < 0 || width < 1 || det_rows < 1 || band_rows < 1 || row_offset < 0 ||
       row_offset + band_rows > det_rows)
     return fail_arg("tk_fft_filter_rows: bad extent / row band");
-  if (n_pad < 2 * width || (n_pad & (n_pad - 1)) != 0)
+  if (n_pad < 2 * width || (n_pad & (n_pad - 1)) != 0 || n_pad < 2)
     return fail_arg("tk_fft_filter_rows: n_pad must be a power of two >= 2*width");
   if (n_pad > kMaxPad) return fail_arg("tk_fft_filter_rows: n_pad above 8192 is not supported");
   if (n_rows == 0) return TK_OK;
   cudaStream_t st = as_stream(stream);
-  const int half = n_pad / 2;
-  // twiddles and folded weights, float64 on the host
-  std::vector<float> host(2 * half + half + 1);
+  // twiddles (full circle) and folded weights, float64 on the host
+  std::vector<float> host(2 * n_pad + n_pad / 2 + 1);
   const double two_pi = 6.283185307179586476925286766559;
-  for (int k = 0; k < half; ++k) {
-    host[2 * k] = (float)cos(-two_pi * k / n_pad);
-    host[2 * k + 1] = (float)sin(-two_pi * k / n_pad);
+  for (int m = 0; m < n_pad; ++m) {
+    host[2 * m] = (float)cos(-two_pi * m / n_pad);
+    host[2 * m + 1] = (float)sin(-two_pi * m / n_pad);
   }
-  for (int k = 0; k <= half; ++k) host[2 * half + k] = (float)(half_weights[k] * scale / n_pad);
+  for (int k = 0; k <= n_pad / 2; ++k) host[2 * n_pad + k] = (float)(half_weights[k] * scale / n_pad);
   Scratch d;
   TK_TRY_CUDA(upload(d, host.data(), sizeof(float) * host.size(), st));
   FilterParams p;
@@ -151,23 +266,32 @@ extern "C" int tk_fft_filter_rows_ex(const float *in, long long n_rows, int widt
   p.row_offset = row_offset;
   p.det_rows = det_rows;
   p.n_pad = n_pad;
-  int lg = 0;
-  while ((1 << lg) < n_pad) ++lg;
-  p.log2n = lg;
   p.tw = reinterpret_cast<const float2 *>(d.as<float>());
-  p.wgt = d.as<float>() + 2 * half;
+  p.wgt = d.as<float>() + 2 * n_pad;
   p.sdd = (float)sdd;
   p.du = (float)du;
   p.dv = (float)dv;
-  const size_t smem = sizeof(float2) * n_pad + sizeof(float2) * half + sizeof(float) * (half + 1);
-  if (smem > 48 * 1024)
-    TK_TRY_CUDA(cudaFuncSetAttribute(fft_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int threads = std::max(32, std::min(256, half));
-  const long long pairs = (n_rows + 1) / 2;
-  const int per_sm = std::max(1, (int)std::min<size_t>(8, (200 * 1024) / smem));
-  const unsigned grid = (unsigned)std::min<long long>(pairs, (long long)sm_count() * per_sm);
-  fft_filter_kernel<<<grid, threads, smem, st>>>(p);
-  TK_LAUNCHED("fft_filter_kernel");
+  const size_t smem = sizeof(float2) * 2 * n_pad + sizeof(float) * (n_pad / 2 + 1);
+  int lg = 0;
+  while ((1 << lg) < n_pad) ++lg;
+  cudaError_t e;
+  switch (lg) {
+    case 1: e = launch_filter<1>(p, smem, st); break;
+    case 2: e = launch_filter<2>(p, smem, st); break;
+    case 3: e = launch_filter<3>(p, smem, st); break;
+    case 4: e = launch_filter<4>(p, smem, st); break;
+    case 5: e = launch_filter<5>(p, smem, st); break;
+    case 6: e = launch_filter<6>(p, smem, st); break;
+    case 7: e = launch_filter<7>(p, smem, st); break;
+    case 8: e = launch_filter<8>(p, smem, st); break;
+    case 9: e = launch_filter<9>(p, smem, st); break;
+    case 10: e = launch_filter<10>(p, smem, st); break;
+    case 11: e = launch_filter<11>(p, smem, st); break;
+    case 12: e = launch_filter<12>(p, smem, st); break;
+    default: e = launch_filter<13>(p, smem, st); break;
+  }
+  if (e != cudaSuccess) return check_cuda(e, "fft_filter_kernel");
+  count_launch();
   return TK_OK;
 }
 
