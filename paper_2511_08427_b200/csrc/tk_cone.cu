@@ -590,6 +590,139 @@ __global__ void __launch_bounds__(kBpBX *kBpBY) cone_bp_kernel(const BpParams p)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Quad-layout back projector ("quad", default).
+//
+// The (band) sinogram is first rewritten as tap quads: for every detector cell
+// (r0, c0) with r0 in [-2, R], c0 in [-2, C] the float4
+//   Q[v][r0+2][c0+2] = (S[r0][c0], S[r0][c0+1], S[r0+1][c0], S[r0+1][c0+1]),
+// S = 0 outside the detector.  One 16-byte load then yields all four bilinear
+// taps of an update, the zero border replaces every per-tap range test
+// (reference _kernels.py:308-317), and an out-of-range row index is simply
+// clamped onto the all-zero quads of rows -2 / R.  A warp covers an 8x4 (x, y)
+// voxel tile (compact detector footprint) and each thread ZB voxels along z.
+// ---------------------------------------------------------------------------
+constexpr int kQuadPad = 2;
+constexpr int kBqBX = 8, kBqBY = 32;
+
+__global__ void quadify_kernel(const float *__restrict__ sino, int n_views, int rows, int cols,
+                               float4 *__restrict__ quads) {
+  const int qc = cols + 1 + kQuadPad, qr = rows + 1 + kQuadPad;
+  const long long total = (long long)n_views * qr * qc;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % qc) - kQuadPad;
+    const long long t = i / qc;
+    const int r0 = (int)(t % qr) - kQuadPad;
+    const int v = (int)(t / qr);
+    const float *s = sino + (long long)v * rows * cols;
+    const bool ca = (unsigned)c0 < (unsigned)cols, cb = (unsigned)(c0 + 1) < (unsigned)cols;
+    const bool ra = (unsigned)r0 < (unsigned)rows, rb = (unsigned)(r0 + 1) < (unsigned)rows;
+    float4 q;
+    q.x = (ra && ca) ? __ldg(s + (long long)r0 * cols + c0) : 0.f;
+    q.y = (ra && cb) ? __ldg(s + (long long)r0 * cols + c0 + 1) : 0.f;
+    q.z = (rb && ca) ? __ldg(s + (long long)(r0 + 1) * cols + c0) : 0.f;
+    q.w = (rb && cb) ? __ldg(s + (long long)(r0 + 1) * cols + c0 + 1) : 0.f;
+    quads[i] = q;
+  }
+}
+
+template <int ZB, bool ZINV, bool WEIGHTED>
+__global__ void __launch_bounds__(kBqBX *kBqBY) cone_bp_quad_kernel(const BpParams p,
+                                                                   const float4 *__restrict__ quads) {
+  __shared__ ConeVoxView sv[kBpChunk];
+  const int ix = blockIdx.x * kBqBX + threadIdx.x;
+  const int iy = blockIdx.y * kBqBY + threadIdx.y;
+  const int zl0 = blockIdx.z * ZB;
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx;
+  const float yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  const int tid = threadIdx.y * kBqBX + threadIdx.x;
+  const int qc = p.cols + 1 + kQuadPad;                 // quads per row
+  const int rmax = p.band_rows;                          // last (all-zero) quad row index r0
+  const long long qview = (long long)(p.band_rows + 1 + kQuadPad) * qc;
+  const float colmax = (float)(p.cols - 1);
+
+  float acc[ZB];
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) acc[k] = 0.f;
+
+  for (int v0 = 0; v0 < p.n_views; v0 += kBpChunk) {
+    const int nch = min(kBpChunk, p.n_views - v0);
+    __syncthreads();
+    for (int i = tid; i < nch * 12; i += kBqBX * kBqBY)
+      reinterpret_cast<float *>(sv)[i] = __ldg(reinterpret_cast<const float *>(p.views + v0) + i);
+    __syncthreads();
+    if (!active) continue;
+    for (int j = 0; j < nch; ++j) {
+      const ConeVoxView &V = sv[j];
+      const float4 *qv = quads + (long long)(v0 + j) * qview;
+      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+      if (ZINV) {
+        if (!(w0 > (float)kTiny)) continue;  // _kernels.py:297-298
+        const float rw = 1.f / w0;
+        const float fc = fmaf(a0, rw, p.cu);
+        const float flc = floorf(fc);
+        if (!(flc >= -1.f && flc <= colmax)) continue;  // both column taps off the detector
+        const float wc = fc - flc;
+        float q = 1.f;
+        if (WEIGHTED) {  // (sid / w)^2, _kernels.py:318-320
+          q = p.sid * rw;
+          q *= q;
+        }
+        const float g0 = q * (1.f - wc), g1 = q * wc;
+        const float4 *col = qv + ((int)flc + kQuadPad);
+        const float fr0 = fmaf(b0, rw, p.cv);
+        const float dr = V.b[2] * rw;
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float flr = floorf(fr);
+          const int r0 = min(max((int)flr, -kQuadPad), rmax);
+          const float4 t = __ldg(col + (unsigned)((r0 + kQuadPad) * qc));  // 32-bit offset
+          const float top = fmaf(g1, t.y, g0 * t.x);
+          const float bot = fmaf(g1, t.w, g0 * t.z);
+          acc[k] += fmaf(fr - flr, bot - top, top);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float kf = (float)k;
+          const float w = fmaf(kf, V.w[2], w0);
+          if (!(w > (float)kTiny)) continue;
+          const float rw = 1.f / w;
+          const float fc = fmaf(fmaf(kf, V.a[2], a0), rw, p.cu);
+          const float fr = fmaf(fmaf(kf, V.b[2], b0), rw, p.cv);
+          const float flc = floorf(fc), flr = floorf(fr);
+          const int c0 = min(max((int)flc, -kQuadPad), p.cols);
+          const int r0 = min(max((int)flr, -kQuadPad), rmax);
+          const float4 t = __ldg(qv + (long long)(r0 + kQuadPad) * qc + (c0 + kQuadPad));
+          const float wc = fc - flc;
+          const float top = lerpf(t.x, t.y, wc), bot = lerpf(t.z, t.w, wc);
+          float val = lerpf(top, bot, fr - flr);
+          if (WEIGHTED) {
+            const float q = p.sid * rw;
+            val *= q * q;
+          }
+          acc[k] += val;
+        }
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
 // Texture-gather variant: the (band) sinogram lives in a layered CUDA array
 // (layer = view); each update fetches its 2x2 tap quad with one TLD4, the
 // zero outside the detector comes from border addressing, and the bilinear
@@ -864,13 +997,39 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
 }
 
 // Back-projector algorithm: TK_BP_ALGO = ldg (default) | tex | hwtex.
-enum class BpAlgo { kLdg, kTex, kHwTex };
+enum class BpAlgo { kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
+  if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
-  return BpAlgo::kLdg;
+  return BpAlgo::kQuad;
+}
+
+constexpr int kBqZB = 16;
+
+static int launch_bp_quad(BpParams p, bool weighted, bool zinv, cudaStream_t st) {
+  const long long qview = (long long)(p.band_rows + 1 + kQuadPad) * (p.cols + 1 + kQuadPad);
+  const long long nq = qview * p.n_views;
+  Scratch quads;
+  TK_TRY_CUDA(quads.alloc(sizeof(float4) * nq, st));
+  const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(nq, 256), (long long)sm_count() * 32);
+  quadify_kernel<<<qgrid, 256, 0, st>>>(p.sino, p.n_views, p.band_rows, p.cols, quads.as<float4>());
+  TK_LAUNCHED("quadify_kernel");
+  dim3 block(kBqBX, kBqBY);
+  dim3 grid(ceil_div(p.nx, kBqBX), ceil_div(p.ny, kBqBY), ceil_div(p.z_count, kBqZB));
+  const float4 *q = quads.as<float4>();
+  if (zinv && weighted)
+    cone_bp_quad_kernel<kBqZB, true, true><<<grid, block, 0, st>>>(p, q);
+  else if (zinv)
+    cone_bp_quad_kernel<kBqZB, true, false><<<grid, block, 0, st>>>(p, q);
+  else if (weighted)
+    cone_bp_quad_kernel<kBqZB, false, true><<<grid, block, 0, st>>>(p, q);
+  else
+    cone_bp_quad_kernel<kBqZB, false, false><<<grid, block, 0, st>>>(p, q);
+  TK_LAUNCHED("cone_bp_quad_kernel");
+  return TK_OK;
 }
 
 template <int ZB, bool ZINV>
@@ -968,9 +1127,11 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   constexpr int ZB = 8;
   dim3 block(kBpBX, kBpBY);
   dim3 grid(ceil_div(nx, kBpBX), ceil_div(ny, kBpBY), ceil_div(z_count, ZB));
-  const BpAlgo algo = n_views <= 2048 ? bp_algo() : BpAlgo::kLdg;  // layered arrays: <= 2048 layers
-  TexLease lease;
   p.tex = 0;
+  BpAlgo algo = bp_algo();
+  if (algo == BpAlgo::kQuad) return launch_bp_quad(p, weighted != 0, zinv, st);
+  if (n_views > 2048) algo = BpAlgo::kLdg;  // layered arrays hold <= 2048 layers
+  TexLease lease;
   if (algo != BpAlgo::kLdg) {
     TK_TRY_CUDA(tex_acquire(sino, cols, band_rows, n_views,
                             algo == BpAlgo::kHwTex ? TexKind::kLayeredLinear : TexKind::kLayeredPoint,

@@ -24,8 +24,8 @@ from paper_2511_08427_b200.projectors import bp_tensor, fp_tensor  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--views", type=int, default=720)
 ap.add_argument("--reps", type=int, default=3)
-ap.add_argument("--fp", default="ldg,tex,hwtex")
-ap.add_argument("--bp", default="ldg,tex,hwtex")
+ap.add_argument("--fp", default="ldg2,ldg,tex,hwtex")
+ap.add_argument("--bp", default="quad,ldg,tex,hwtex")
 ap.add_argument("--out", default="")
 a = ap.parse_args()
 
