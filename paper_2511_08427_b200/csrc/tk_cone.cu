@@ -272,10 +272,18 @@ __device__ __forceinline__ float interp_cell(const CellTaps &t, float wa, float 
 __global__ void __launch_bounds__(kFp2BX *kFp2BY)
     cone_fp2_kernel(const float *__restrict__ volA, const float *__restrict__ volB, int nx, int ny,
                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
-                    int rows, int cols, double step, float *__restrict__ out) {
-  const int c = blockIdx.x * kFp2BX + threadIdx.x;
-  const int r = blockIdx.y * kFp2BY + threadIdx.y;
-  const int v = blockIdx.z;
+                    int rows, int cols, int n_views, double step, float *__restrict__ out) {
+  // 1D grid, view-major within a detector row band: consecutive CTAs cover the
+  // same rows of successive views, so the CTAs resident at any time sample the
+  // same thin z-slab of the volume (which then stays in L2 across views).
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r = rb * kFp2BY + threadIdx.y;
   if (c >= cols || r >= rows) return;
   float *dst = out + ((long long)v * rows + r) * cols + c;
   const Fp2View W = views[v];
@@ -628,7 +636,7 @@ __global__ void quadify_kernel(const float *__restrict__ sino, int n_views, int 
 }
 
 template <int ZB, bool ZINV, bool WEIGHTED>
-__global__ void __launch_bounds__(kBqBX *kBqBY) cone_bp_quad_kernel(const BpParams p,
+__global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_quad_kernel(const BpParams p,
                                                                    const float4 *__restrict__ quads) {
   __shared__ ConeVoxView sv[kBpChunk];
   const int ix = blockIdx.x * kBqBX + threadIdx.x;
@@ -677,15 +685,27 @@ __global__ void __launch_bounds__(kBqBX *kBqBY) cone_bp_quad_kernel(const BpPara
         const float4 *col = qv + ((int)flc + kQuadPad);
         const float fr0 = fmaf(b0, rw, p.cv);
         const float dr = V.b[2] * rw;
+        // batches of 8 independent 16-byte loads in flight per thread
 #pragma unroll
-        for (int k = 0; k < ZB; ++k) {
-          const float fr = fmaf((float)k, dr, fr0);
-          const float flr = floorf(fr);
-          const int r0 = min(max((int)flr, -kQuadPad), rmax);
-          const float4 t = __ldg(col + (unsigned)((r0 + kQuadPad) * qc));  // 32-bit offset
-          const float top = fmaf(g1, t.y, g0 * t.x);
-          const float bot = fmaf(g1, t.w, g0 * t.z);
-          acc[k] += fmaf(fr - flr, bot - top, top);
+        for (int k0 = 0; k0 < ZB; k0 += 8) {
+          unsigned off[8];
+          float wr[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float fr = fmaf((float)(k0 + i), dr, fr0);
+            const float flr = floorf(fr);
+            off[i] = (unsigned)((min(max((int)flr, -kQuadPad), rmax) + kQuadPad) * qc);
+            wr[i] = fr - flr;
+          }
+          float4 t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = __ldg(col + off[i]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float top = fmaf(g1, t[i].y, g0 * t[i].x);
+            const float bot = fmaf(g1, t[i].w, g0 * t[i].z);
+            acc[k0 + i] += fmaf(wr[i], bot - top, top);
+          }
         }
       } else {
 #pragma unroll
@@ -934,9 +954,11 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
     TK_LAUNCHED("pad_margin_kernel");
   }
   dim3 block(kFp2BX, kFp2BY);
-  dim3 grid(ceil_div(cols, kFp2BX), ceil_div(rows, kFp2BY), n_views);
-  cone_fp2_kernel<<<grid, block, 0, st>>>(volA.as<float>(), volB.as<float>(), nx, ny, nz, sx, sy, sz,
-                                          dviews.as<Fp2View>(), rows, cols, step, out);
+  const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
+  if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
+  cone_fp2_kernel<<<(unsigned)nblocks, block, 0, st>>>(volA.as<float>(), volB.as<float>(), nx, ny, nz,
+                                                       sx, sy, sz, dviews.as<Fp2View>(), rows, cols,
+                                                       n_views, step, out);
   TK_LAUNCHED("cone_fp2_kernel");
   return TK_OK;
 }

@@ -426,4 +426,4 @@ def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
             z0, z1 = D.shard_bounds(32, world, rank)
             r0, r1 = D.row_band(geom, z0, z1)
             slab = bp_cone_tensor_ex(y[:, r0:r1].contiguous(), geom, True, r0, z0, z1 - z0)
-            assert rel(slab, full[z0:z1].cpu().numpy()) < 1e-6
+            assert rel(slab, full[z0:z1].cpu().numpy()) < 1e-5  # fp32 row-shift rounding
