@@ -269,7 +269,8 @@ __device__ __forceinline__ float interp_cell(const CellTaps &t, float wa, float 
   return fmaf(wz, hi - lo, lo);
 }
 
-__global__ void __launch_bounds__(kFp2BX *kFp2BY)
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     cone_fp2_kernel(const float *__restrict__ volA, const float *__restrict__ volB, int nx, int ny,
                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
                     int rows, int cols, int n_views, double step, float *__restrict__ out) {
@@ -326,6 +327,192 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY)
     acc = fmaf(rs.last, interp_cell(t, fa - la, fb - lb, fz - lz), acc);
   }
   *dst = acc * (float)step;
+}
+
+// ---------------------------------------------------------------------------
+// Forward projection, quad-tap variant ("ldg4", default).
+//
+// The ncu capture of cone_fp2_kernel shows the L1 tag stage (output
+// wavefronts, ~80% of peak) as the limit: 8 scalar loads per cell, each
+// touching 2-3 lines.  Here every margin-padded cell (z, b, a) of the
+// orientation copy stores its four in-slice taps as one float4
+//   Q[z][b][a] = (V[z][b][a], V[z][b][a+1], V[z][b+1][a], V[z][b+1][a+1]),
+// so a cell is 2 LDG.128 (slices z and z+1) instead of 8 LDG.32.
+// Same traversal, ordering, arithmetic order of weights as cone_fp2_kernel.
+// ---------------------------------------------------------------------------
+__global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
+                                   float4 *__restrict__ q) {
+  constexpr int m = kFpMargin;
+  const int na = swap_xy ? ny : nx, nb = swap_xy ? nx : ny;
+  const int pa = na + 2 * m, pb = nb + 2 * m, pz = nz + 2 * m;
+  const long long total = (long long)pz * pb * pa;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(i % pa) - m;
+    const long long t = i / pa;
+    const int b = (int)(t % pb) - m;
+    const int z = (int)(t / pb) - m;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int aa = a + (j & 1), bb = b + (j >> 1);
+      float val = 0.f;
+      if ((unsigned)z < (unsigned)nz && (unsigned)aa < (unsigned)na && (unsigned)bb < (unsigned)nb) {
+        const int x = swap_xy ? bb : aa, y = swap_xy ? aa : bb;
+        val = __ldg(vol + ((long long)z * ny + y) * nx + x);
+      }
+      v[j] = val;
+    }
+    q[i] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
+    cone_fp4_kernel(const float4 *__restrict__ qA, const float4 *__restrict__ qB, int nx, int ny,
+                    int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
+                    int rows, int cols, int n_views, double step, float *__restrict__ out) {
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r = rb * kFp2BY + threadIdx.y;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  const float4 *q = W.swap ? qB : qA;
+  const int na = W.swap ? ny : nx, nb = W.swap ? nx : ny;
+  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const int pa = na + 2 * kFpMargin;
+  const int ps = (nb + 2 * kFpMargin) * pa;
+  int cell = -1;
+  float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
+  float acc = 0.f;
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k <= nfull; ++k, kf += 1.f) {
+    const bool last = k == nfull;
+    const float kk = last ? (float)nfull + 0.5f * rs.last : kf;
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
+    const int id = (int)lz * ps + (int)lb * pa + (int)la;
+    if (id != cell) {
+      cell = id;
+      lo4 = __ldg(q + id);
+      hi4 = __ldg(q + id + ps);
+    }
+    const float wa = fa - la, wb = fb - lb, wz = fz - lz;
+    const float s0 = lerpf(lerpf(lo4.x, lo4.y, wa), lerpf(lo4.z, lo4.w, wa), wb);
+    const float s1 = lerpf(lerpf(hi4.x, hi4.y, wa), lerpf(hi4.z, hi4.w, wa), wb);
+    const float val = lerpf(s0, s1, wz);
+    acc = last ? fmaf(rs.last, val, acc) : acc + val;
+  }
+  *dst = acc * (float)step;
+}
+
+// Two rays per thread (detector rows r and r+1 of the same column): the two
+// independent sample chains double the loads in flight per warp, hiding L1/L2
+// latency without more resident warps.  Same arithmetic as cone_fp2_kernel.
+struct RayMarch {
+  float ea, eb, ez;
+  int nfull;
+  float last;
+  int cell;
+  CellTaps t;
+  float acc;
+  bool live;
+};
+
+__device__ __forceinline__ void march_sample(RayMarch &m, const float *__restrict__ vol, float kf,
+                                             float ga, float gb, float gz, int pa, int ps) {
+  const float fa = fmaf(kf, ga, m.ea), fb = fmaf(kf, gb, m.eb), fz = fmaf(kf, gz, m.ez);
+  const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
+  const int id = (int)lz * ps + (int)lb * pa + (int)la;
+  if (id != m.cell) {
+    m.cell = id;
+    load_cell(vol + id, pa, ps, m.t);
+  }
+  m.acc += interp_cell(m.t, fa - la, fb - lb, fz - lz);
+}
+
+__device__ __forceinline__ void march_last(RayMarch &m, const float *__restrict__ vol, float ga,
+                                           float gb, float gz, int pa, int ps) {
+  const float kf = (float)m.nfull + 0.5f * m.last;
+  const float fa = fmaf(kf, ga, m.ea), fb = fmaf(kf, gb, m.eb), fz = fmaf(kf, gz, m.ez);
+  const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
+  const int id = (int)lz * ps + (int)lb * pa + (int)la;
+  if (id != m.cell) load_cell(vol + id, pa, ps, m.t);
+  m.acc = fmaf(m.last, interp_cell(m.t, fa - la, fb - lb, fz - lz), m.acc);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
+    cone_fp2r_kernel(const float *__restrict__ volA, const float *__restrict__ volB, int nx, int ny,
+                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
+                     int rows, int cols, int n_views, double step, float *__restrict__ out) {
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r0 = rb * (2 * kFp2BY) + 2 * threadIdx.y;  // rows r0 and r0 + 1
+  if (c >= cols || r0 >= rows) return;
+  const Fp2View W = views[v];
+  const bool swap = W.swap != 0;
+  const float *vol = swap ? volB : volA;
+  const int na = swap ? ny : nx, nb = swap ? nx : ny;
+  const int pa = na + 2 * kFpMargin;
+  const int ps = (nb + 2 * kFpMargin) * pa;
+  RayMarch m[2];
+  float g[2][3];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    RaySetup rs;
+    m[j].live = (r0 + j) < rows && cone_ray_setup(W.ray, r0 + j, c, nx, ny, nz, sx, sy, sz, step, rs);
+    m[j].cell = -1;
+    m[j].t = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    m[j].acc = 0.f;
+    m[j].nfull = m[j].live ? rs.n - 1 : 0;
+    m[j].last = m[j].live ? rs.last : 0.f;
+    m[j].ea = m[j].live ? (swap ? rs.ey : rs.ex) + (kFpMargin - 1) : 0.f;
+    m[j].eb = m[j].live ? (swap ? rs.ex : rs.ey) + (kFpMargin - 1) : 0.f;
+    m[j].ez = m[j].live ? rs.ez + (kFpMargin - 1) : 0.f;
+    g[j][0] = m[j].live ? (swap ? rs.gy : rs.gx) : 0.f;
+    g[j][1] = m[j].live ? (swap ? rs.gx : rs.gy) : 0.f;
+    g[j][2] = m[j].live ? rs.gz : 0.f;
+  }
+  const float ga = g[0][0], gb = g[0][1], gz = g[0][2];
+  const float ga1 = g[1][0], gb1 = g[1][1], gz1 = g[1][2];
+  const int n0 = m[0].live ? m[0].nfull : 0, n1 = m[1].live ? m[1].nfull : 0;
+  const int nmin = min(n0, n1), nmax = max(n0, n1);
+  float kf = 0.5f;
+  int k = 0;
+  for (; k < nmin; ++k, kf += 1.f) {
+    march_sample(m[0], vol, kf, ga, gb, gz, pa, ps);
+    march_sample(m[1], vol, kf, ga1, gb1, gz1, pa, ps);
+  }
+  for (; k < nmax; ++k, kf += 1.f) {
+    if (k < n0) march_sample(m[0], vol, kf, ga, gb, gz, pa, ps);
+    if (k < n1) march_sample(m[1], vol, kf, ga1, gb1, gz1, pa, ps);
+  }
+  if (m[0].live) march_last(m[0], vol, ga, gb, gz, pa, ps);
+  if (m[1].live) march_last(m[1], vol, ga1, gb1, gz1, pa, ps);
+  float *dst = out + ((long long)v * rows + r0) * cols + c;
+  dst[0] = m[0].live ? m[0].acc * (float)step : 0.f;
+  if (r0 + 1 < rows) dst[cols] = m[1].live ? m[1].acc * (float)step : 0.f;
 }
 
 // Texture-gather variant: the volume lives in a layered CUDA array (layer =
@@ -913,15 +1100,56 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg2 (default) | ldg | tex | hwtex.
-enum class FpAlgo { kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg4 (default) | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg4, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
   if (e && !strcmp(e, "ldg")) return FpAlgo::kLdg;
+  if (e && !strcmp(e, "ldg2")) return FpAlgo::kLdg2;
   if (e && !strcmp(e, "tex")) return FpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
-  return FpAlgo::kLdg2;
+  return FpAlgo::kLdg4;
+}
+
+static int launch_fp4(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                      const double *sources, const double *minv, int n_views, int rows, int cols,
+                      double step, float *out, cudaStream_t st) {
+  std::vector<Fp2View> hv(n_views);
+  bool need_a = false, need_b = false;
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
+    const double ux = fabs(minv[9 * i + 0] / sx), uy = fabs(minv[9 * i + 3] / sy);
+    hv[i].swap = uy > ux ? 1 : 0;
+    hv[i].pad = 0;
+    (hv[i].swap ? need_b : need_a) = true;
+  }
+  Scratch dviews, qA, qB;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
+  constexpr int m2 = 2 * kFpMargin;
+  const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
+  if (need_a) {
+    TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
+    quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, qA.as<float4>());
+    TK_LAUNCHED("quad_volume_kernel");
+  }
+  if (need_b) {
+    TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
+    quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 1, qB.as<float4>());
+    TK_LAUNCHED("quad_volume_kernel");
+  }
+  dim3 block(kFp2BX, kFp2BY);
+  const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
+  if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
+  const char *mb = getenv("TK_FP2_MINB");
+  const int minb = mb ? atoi(mb) : 10;
+  auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
+  kern<<<(unsigned)nblocks, block, 0, st>>>(qA.as<float4>(), qB.as<float4>(), nx, ny, nz, sx, sy, sz,
+                                            dviews.as<Fp2View>(), rows, cols, n_views, step, out);
+  TK_LAUNCHED("cone_fp4_kernel");
+  return TK_OK;
 }
 
 static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
@@ -954,11 +1182,19 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
     TK_LAUNCHED("pad_margin_kernel");
   }
   dim3 block(kFp2BX, kFp2BY);
-  const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
+  // TK_FP2_RAYS: rays per thread (1 or 2); TK_FP2_MINB: min resident CTAs per SM
+  // (register cap) -- 10 (default), 12, 16
+  const char *rp = getenv("TK_FP2_RAYS");
+  const int rays = rp ? atoi(rp) : 1;
+  const char *mb = getenv("TK_FP2_MINB");
+  const int minb = mb ? atoi(mb) : 10;
+  const long long nblocks =
+      (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY * (rays == 2 ? 2 : 1)) * n_views;
   if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-  cone_fp2_kernel<<<(unsigned)nblocks, block, 0, st>>>(volA.as<float>(), volB.as<float>(), nx, ny, nz,
-                                                       sx, sy, sz, dviews.as<Fp2View>(), rows, cols,
-                                                       n_views, step, out);
+  auto kern = rays == 2 ? (minb >= 12 ? cone_fp2r_kernel<12> : (minb >= 8 ? cone_fp2r_kernel<8> : cone_fp2r_kernel<6>))
+                        : (minb >= 16 ? cone_fp2_kernel<16> : (minb >= 12 ? cone_fp2_kernel<12> : cone_fp2_kernel<10>));
+  kern<<<(unsigned)nblocks, block, 0, st>>>(volA.as<float>(), volB.as<float>(), nx, ny, nz, sx, sy, sz,
+                                            dviews.as<Fp2View>(), rows, cols, n_views, step, out);
   TK_LAUNCHED("cone_fp2_kernel");
   return TK_OK;
 }
@@ -977,6 +1213,8 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
+  if (!adjoint && algo == FpAlgo::kLdg4)
+    return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo != FpAlgo::kLdg) {

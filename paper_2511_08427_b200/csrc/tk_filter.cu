@@ -87,69 +87,68 @@ __device__ __forceinline__ float preweight(const FilterParams &p, long long row,
 // Source of stage inputs: 0 = shared buffer, 1 = global rows (first forward
 // stage), 2 = shared buffer x weights, conjugated (first inverse stage).
 // Destination: 0 = shared buffer, 1 = global rows conjugated (last inverse stage).
+//
+// Every thread owns 8 complex values per stage: one radix-8 butterfly, two
+// radix-4 or four radix-2 butterflies (blockDim = N/8), so the register
+// footprint is the same 8 values in every stage.
 template <int R>
 __device__ __forceinline__ void stockham_stage(float2 *x, const float2 *tw, int N, int Ns, int src,
                                                int dst, const FilterParams &p, const float *ia,
                                                const float *ib, long long ra, long long rb,
                                                bool has_b, float *oa, float *ob, const float *wgt) {
+  constexpr int kB = 8 / R;  // butterflies per thread
   const int nb = N / R;
   const int tstride = N / (Ns * R);
+  const bool active = (int)threadIdx.x * kB < nb;
   float2 v[8];
-  // butterflies of this thread: blockDim >= N/8, so at most 8/R of them
-  constexpr int kMaxB = 8 / R;
-  int jj[kMaxB];
-  float2 vv[kMaxB][R];
-  int cnt = 0;
+  if (active) {
 #pragma unroll
-  for (int c = 0; c < kMaxB; ++c) {
-    const int j = threadIdx.x + c * blockDim.x;
-    if (j >= nb) break;
-    ++cnt;
-    jj[c] = j;
-    const int k = j % Ns;
+    for (int c = 0; c < kB; ++c) {
+      const int j = threadIdx.x * kB + c;
+      const int k = j % Ns;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int e = j + r * nb;
-      float2 z;
-      if (src == 1) {
-        float a = 0.f, b = 0.f;
-        if (e < p.width) {
-          a = __ldg(ia + e) * preweight(p, ra, e);
-          if (has_b) b = __ldg(ib + e) * preweight(p, rb, e);
+      for (int r = 0; r < R; ++r) {
+        const int e = j + r * nb;
+        float2 z;
+        if (src == 1) {
+          float a = 0.f, b = 0.f;
+          if (e < p.width) {
+            a = __ldg(ia + e) * preweight(p, ra, e);
+            if (has_b) b = __ldg(ib + e) * preweight(p, rb, e);
+          }
+          z = make_float2(a, b);
+        } else {
+          z = x[e];
+          if (src == 2) {
+            const float w = wgt[e <= N / 2 ? e : N - e];
+            z = make_float2(z.x * w, -z.y * w);
+          }
         }
-        z = make_float2(a, b);
-      } else {
-        z = x[e];
-        if (src == 2) {
-          const float w = wgt[e <= N / 2 ? e : N - e];
-          z = make_float2(z.x * w, -z.y * w);
-        }
+        v[c * R + r] = (r > 0 && Ns > 1) ? cmul(z, tw[r * k * tstride]) : z;
       }
-      v[r] = (r > 0 && Ns > 1) ? cmul(z, tw[r * k * tstride]) : z;
+      if (R == 8) dft8(v);
+      if (R == 4) dft4(v[c * 4], v[c * 4 + 1], v[c * 4 + 2], v[c * 4 + 3]);
+      if (R == 2) dft2(v + c * 2);
     }
-    if (R == 8) dft8(v);
-    if (R == 4) dft4(v[0], v[1], v[2], v[3]);
-    if (R == 2) dft2(v);
-#pragma unroll
-    for (int r = 0; r < R; ++r) vv[c][r] = v[r];
   }
   __syncthreads();  // every thread has read its inputs (in-place buffer)
+  if (active) {
 #pragma unroll
-  for (int c = 0; c < kMaxB; ++c) {
-    if (c >= cnt) break;
-    const int j = jj[c];
-    const int k = j % Ns;
-    const int base = (j / Ns) * Ns * R + k;
+    for (int c = 0; c < kB; ++c) {
+      const int j = threadIdx.x * kB + c;
+      const int k = j % Ns;
+      const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int o = base + r * Ns;
-      if (dst == 1) {
-        if (o < p.width) {
-          oa[o] = vv[c][r].x;
-          if (has_b) ob[o] = -vv[c][r].y;
+      for (int r = 0; r < R; ++r) {
+        const int o = base + r * Ns;
+        if (dst == 1) {
+          if (o < p.width) {
+            oa[o] = v[c * R + r].x;
+            if (has_b) ob[o] = -v[c * R + r].y;
+          }
+        } else {
+          x[o] = v[c * R + r];
         }
-      } else {
-        x[o] = vv[c][r];
       }
     }
   }
@@ -190,7 +189,7 @@ constexpr int filter_threads() {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(filter_threads<LOGN>()) fft_filter_kernel(const FilterParams p) {
+__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 2 : 1)) fft_filter_kernel(const FilterParams p) {
   extern __shared__ float smem[];
   constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);
