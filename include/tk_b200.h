@@ -88,6 +88,18 @@ int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz,
                        double sy, double sx, const double *sources,
                        const double *minv, int n_views, int rows, int cols,
                        double step, float *out, void *stream);
+/* Forward-projection plan (no reference counterpart): the per-volume
+ * preprocessing of tk_forward_cone_3d (zero-margin quad-tap copies of the
+ * volume in two orientations) done once, then any number of view blocks
+ * projected from it -- e.g. view chunks whose D2H copies overlap the next
+ * chunk's kernel.  *plan is an opaque handle; destroy frees it stream-ordered
+ * on `stream` (the caller orders other streams' uses before that). */
+int tk_fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, double sy,
+                      double sx, void **plan, void *stream);
+int tk_fp_plan_project(void *plan, const double *sources, const double *minv,
+                       int n_views, int rows, int cols, double step, float *out,
+                       void *stream);
+int tk_fp_plan_destroy(void *plan, void *stream);
 /* replaces _kernels.back_cone_3d (_kernels.py:281-322) as called from
  * projectors.back_project_cone_3d (projectors.py:228-248).
  * sino (V,rows,cols) device; mats host float64 (V,3,4); out (nz,ny,nx). */

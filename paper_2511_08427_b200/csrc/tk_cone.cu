@@ -930,6 +930,206 @@ __global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_quad_kernel(const BpP
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory staged back projector ("smem", default for z-invariant
+// trajectories) -- the north star's "detector tiles for a batch of views are
+// staged into shared memory".
+//
+// CTA = 16x16 (x, y) voxel columns x kBsZB z-voxels.  For each batch of kBsNV
+// views, the CTA projects the 8 corners of its voxel box through each view's
+// P (exact bound: central projection of a convex box), and copies the
+// covering detector rectangle (+1 pixel margin) into shared memory with
+// cp.async (zero-filled outside the detector = the reference's per-tap
+// bounds).  The next batch streams in while the current one is consumed
+// (double buffering).  Each update then reads its 4 taps with LDS (L1 data
+// path not involved) -- 128 B/clk/SM of shared-memory bandwidth instead of
+// the ~64 B/clk the L1 load path sustains for 16-byte-per-lane gathers.
+// A view whose rectangle does not fit (extreme magnification) or that has a
+// corner behind the source is gathered straight from global memory instead.
+// ---------------------------------------------------------------------------
+constexpr int kBsTX = 16, kBsTY = 16, kBsZB = 16, kBsNV = 4, kBsCap = 3072;
+
+struct BsRect {
+  int r0, c0, h, w;  // detector rectangle (band-local rows), h*w <= kBsCap, or w = 0: uncached
+};
+
+__device__ __forceinline__ void cp_async4(float *smem_dst, const float *gsrc, bool valid) {
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int bytes = valid ? 4 : 0;  // 0 source bytes -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(gsrc), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Rectangle of the CTA's voxel box in view V (band-local rows); uncached if
+// it does not fit or the box reaches behind the source.
+__device__ __forceinline__ BsRect bs_rect(const ConeVoxView &V, const BpParams &p, float x0, float x1,
+                                          float y0, float y1, float z0, float z1) {
+  float cmin = 1e30f, cmax = -1e30f, rmin = 1e30f, rmax = -1e30f;
+  bool behind = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float x = (i & 1) ? x1 : x0, y = (i & 2) ? y1 : y0, z = (i & 4) ? z1 : z0;
+    const float w = fmaf(V.w[0], x, fmaf(V.w[1], y, fmaf(V.w[2], z, V.w[3])));
+    behind |= !(w > (float)kTiny);
+    const float rw = 1.f / w;
+    const float fc = fmaf(fmaf(V.a[0], x, fmaf(V.a[1], y, fmaf(V.a[2], z, V.a[3]))), rw, p.cu);
+    const float fr = fmaf(fmaf(V.b[0], x, fmaf(V.b[1], y, fmaf(V.b[2], z, V.b[3]))), rw, p.cv);
+    cmin = fminf(cmin, fc);
+    cmax = fmaxf(cmax, fc);
+    rmin = fminf(rmin, fr);
+    rmax = fmaxf(rmax, fr);
+  }
+  BsRect R;
+  // taps floor(f) and floor(f)+1, plus one pixel of rounding margin each side
+  R.c0 = (int)floorf(cmin) - 1;
+  R.r0 = (int)floorf(rmin) - 1;
+  R.w = (int)floorf(cmax) + 3 - R.c0;
+  R.h = (int)floorf(rmax) + 3 - R.r0;
+  if (behind || R.w <= 0 || R.h <= 0 || R.w * R.h > kBsCap || !(cmax - cmin < 1e6f) ||
+      !(rmax - rmin < 1e6f)) {
+    R.w = 0;
+    R.h = 0;
+  }
+  return R;
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(kBsTX *kBsTY, 2) cone_bp_smem_kernel(const BpParams p) {
+  extern __shared__ float smem_bs[];
+  float *tiles = smem_bs;  // [2][kBsNV][kBsCap]
+  __shared__ ConeVoxView sv[2][kBsNV];
+  __shared__ BsRect rect[2][kBsNV];
+  const int tx = threadIdx.x & (kBsTX - 1), ty = threadIdx.x / kBsTX;
+  const int ix = blockIdx.x * kBsTX + tx;
+  const int iy = blockIdx.y * kBsTY + ty;
+  const int zl0 = blockIdx.z * kBsZB;
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx, yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  // the CTA's voxel box in centred index units (clipped to the volume)
+  const float bx0 = (float)(blockIdx.x * kBsTX) - p.cx;
+  const float bx1 = (float)(min((int)(blockIdx.x + 1) * kBsTX, p.nx) - 1) - p.cx;
+  const float by0 = (float)(blockIdx.y * kBsTY) - p.cy;
+  const float by1 = (float)(min((int)(blockIdx.y + 1) * kBsTY, p.ny) - 1) - p.cy;
+  const float bz1 = (float)(p.z_begin + min(zl0 + kBsZB, p.z_count) - 1) - p.cz;
+  const int tid = threadIdx.x;
+  const int nbatch = (p.n_views + kBsNV - 1) / kBsNV;
+
+  float acc[kBsZB];
+#pragma unroll
+  for (int k = 0; k < kBsZB; ++k) acc[k] = 0.f;
+
+  // stage batch `bi` into buffer `buf` (views, rectangles, async tile copies)
+  auto stage = [&](int bi, int buf) {
+    const int v0 = bi * kBsNV;
+    if (tid < kBsNV) {
+      const int v = v0 + tid;
+      if (v < p.n_views) {
+        const ConeVoxView V = p.views[v];
+        sv[buf][tid] = V;
+        rect[buf][tid] = bs_rect(V, p, bx0, bx1, by0, by1, zc0, bz1);
+      } else {
+        rect[buf][tid] = BsRect{0, 0, 0, 0};
+      }
+    }
+    __syncthreads();
+    for (int j = 0; j < kBsNV; ++j) {
+      const BsRect R = rect[buf][j];
+      if (R.w == 0) continue;
+      const float *src = p.sino + (long long)(v0 + j) * p.view_stride;
+      float *dst = tiles + (buf * kBsNV + j) * kBsCap;
+      const int n = R.w * R.h;
+      for (int e = tid; e < n; e += kBsTX * kBsTY) {
+        const int rr = R.r0 + e / R.w, cc = R.c0 + e % R.w;
+        const bool in = (unsigned)rr < (unsigned)p.band_rows && (unsigned)cc < (unsigned)p.cols;
+        cp_async4(dst + e, in ? src + (long long)rr * p.cols + cc : src, in);
+      }
+    }
+    cp_async_commit();
+  };
+
+  stage(0, 0);
+  for (int bi = 0; bi < nbatch; ++bi) {
+    const int buf = bi & 1;
+    if (bi + 1 < nbatch) {
+      __syncthreads();  // buffer buf^1 is no longer read (previous iteration)
+      stage(bi + 1, buf ^ 1);
+      cp_async_wait_prev();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    if (!active) continue;
+    const int v0 = bi * kBsNV;
+    for (int j = 0; j < kBsNV; ++j) {
+      if (v0 + j >= p.n_views) break;
+      const ConeVoxView &V = sv[buf][j];
+      const BsRect R = rect[buf][j];
+      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+      if (!(w0 > (float)kTiny)) continue;
+      const float rw = 1.f / w0;
+      const float fc = fmaf(a0, rw, p.cu);
+      const float flc = floorf(fc);
+      float q = 1.f;
+      if (WEIGHTED) {
+        q = p.sid * rw;
+        q *= q;
+      }
+      const float wc = fc - flc;
+      const float g0 = q * (1.f - wc), g1 = q * wc;
+      const float fr0 = fmaf(b0, rw, p.cv);
+      const float dr = V.b[2] * rw;
+      if (R.w > 0) {
+        const float *t = tiles + (buf * kBsNV + j) * kBsCap;
+        const int cl = min(max((int)flc - R.c0, 0), R.w - 2);
+        const int hmax = R.h - 2;
+#pragma unroll
+        for (int k = 0; k < kBsZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float flr = floorf(fr);
+          const int rl = min(max((int)flr - R.r0, 0), hmax);
+          const float *e = t + rl * R.w + cl;
+          const float top = fmaf(g1, e[1], g0 * e[0]);
+          const float bot = fmaf(g1, e[R.w + 1], g0 * e[R.w]);
+          acc[k] += fmaf(fr - flr, bot - top, top);
+        }
+      } else {  // uncached view: bounded global gathers (reference per-tap bounds)
+        const float *s = p.sino + (long long)(v0 + j) * p.view_stride;
+        const int c0 = (int)flc;
+        const bool ca = (unsigned)c0 < (unsigned)p.cols, cb = (unsigned)(c0 + 1) < (unsigned)p.cols;
+#pragma unroll
+        for (int k = 0; k < kBsZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float flr = floorf(fr);
+          const int r0 = (int)flr;
+          const bool ra = (unsigned)r0 < (unsigned)p.band_rows;
+          const bool rb = (unsigned)(r0 + 1) < (unsigned)p.band_rows;
+          const float *e = s + (long long)r0 * p.cols + c0;
+          const float t00 = (ra && ca) ? __ldg(e) : 0.f, t01 = (ra && cb) ? __ldg(e + 1) : 0.f;
+          const float t10 = (rb && ca) ? __ldg(e + p.cols) : 0.f;
+          const float t11 = (rb && cb) ? __ldg(e + p.cols + 1) : 0.f;
+          const float top = fmaf(g1, t01, g0 * t00);
+          const float bot = fmaf(g1, t11, g0 * t10);
+          acc[k] += fmaf(fr - flr, bot - top, top);
+        }
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < kBsZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
 // Texture-gather variant: the (band) sinogram lives in a layered CUDA array
 // (layer = view); each update fetches its 2x2 tap quad with one TLD4, the
 // zero outside the detector comes from border addressing, and the bilinear
@@ -1112,44 +1312,74 @@ static FpAlgo fp_algo() {
   return FpAlgo::kLdg4;
 }
 
-static int launch_fp4(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
-                      const double *sources, const double *minv, int n_views, int rows, int cols,
-                      double step, float *out, cudaStream_t st) {
-  std::vector<Fp2View> hv(n_views);
-  bool need_a = false, need_b = false;
-  for (int i = 0; i < n_views; ++i) {
-    for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
-    for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
-    const double ux = fabs(minv[9 * i + 0] / sx), uy = fabs(minv[9 * i + 3] / sy);
-    hv[i].swap = uy > ux ? 1 : 0;
-    hv[i].pad = 0;
-    (hv[i].swap ? need_b : need_a) = true;
-  }
-  Scratch dviews, qA, qB;
-  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
+// A forward-projection plan: the two quad-tap orientation copies of one
+// volume, built once and reused by any number of view blocks (the e2e path
+// projects view chunks so their D2H copies overlap the next chunk's kernel).
+struct FpPlan {
+  int nz, ny, nx;
+  double sz, sy, sx;
+  float4 *qA = nullptr, *qB = nullptr;
+};
+
+static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                          FpPlan *plan, cudaStream_t st) {
+  plan->nz = nz;
+  plan->ny = ny;
+  plan->nx = nx;
+  plan->sz = sz;
+  plan->sy = sy;
+  plan->sx = sx;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
-  if (need_a) {
-    TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
-    quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, qA.as<float4>());
-    TK_LAUNCHED("quad_volume_kernel");
+  TK_TRY_CUDA(cudaMallocAsync(&plan->qA, sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(cudaMallocAsync(&plan->qB, sizeof(float4) * ncell, st));
+  quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, plan->qA);
+  TK_LAUNCHED("quad_volume_kernel");
+  quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 1, plan->qB);
+  TK_LAUNCHED("quad_volume_kernel");
+  return TK_OK;
+}
+
+static void fp_plan_free(FpPlan *plan, cudaStream_t st) {
+  if (plan->qA) cudaFreeAsync(plan->qA, st);
+  if (plan->qB) cudaFreeAsync(plan->qB, st);
+  plan->qA = plan->qB = nullptr;
+}
+
+static int fp_plan_project(const FpPlan &pl, const double *sources, const double *minv, int n_views,
+                           int rows, int cols, double step, float *out, cudaStream_t st) {
+  std::vector<Fp2View> hv(n_views);
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
+    // detector u direction (column 0 of M^-1) in voxel units picks the copy
+    const double ux = fabs(minv[9 * i + 0] / pl.sx), uy = fabs(minv[9 * i + 3] / pl.sy);
+    hv[i].swap = uy > ux ? 1 : 0;
+    hv[i].pad = 0;
   }
-  if (need_b) {
-    TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
-    quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 1, qB.as<float4>());
-    TK_LAUNCHED("quad_volume_kernel");
-  }
+  Scratch dviews;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
   dim3 block(kFp2BX, kFp2BY);
   const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
   if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
   const char *mb = getenv("TK_FP2_MINB");
   const int minb = mb ? atoi(mb) : 10;
   auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
-  kern<<<(unsigned)nblocks, block, 0, st>>>(qA.as<float4>(), qB.as<float4>(), nx, ny, nz, sx, sy, sz,
+  kern<<<(unsigned)nblocks, block, 0, st>>>(pl.qA, pl.qB, pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
                                             dviews.as<Fp2View>(), rows, cols, n_views, step, out);
   TK_LAUNCHED("cone_fp4_kernel");
   return TK_OK;
+}
+
+static int launch_fp4(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                      const double *sources, const double *minv, int n_views, int rows, int cols,
+                      double step, float *out, cudaStream_t st) {
+  FpPlan plan;
+  int rc = fp_plan_create(vol, nz, ny, nx, sz, sy, sx, &plan, st);
+  if (rc == TK_OK) rc = fp_plan_project(plan, sources, minv, n_views, rows, cols, step, out, st);
+  fp_plan_free(&plan, st);
+  return rc;
 }
 
 static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
@@ -1257,17 +1487,35 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
 }
 
 // Back-projector algorithm: TK_BP_ALGO = ldg (default) | tex | hwtex.
-enum class BpAlgo { kQuad, kLdg, kTex, kHwTex };
+enum class BpAlgo { kSmem, kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
+  if (e && !strcmp(e, "quad")) return BpAlgo::kQuad;
   if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
-  return BpAlgo::kQuad;
+  return BpAlgo::kSmem;
 }
 
 constexpr int kBqZB = 16;
+
+static int launch_bp_smem(const BpParams &p, bool weighted, cudaStream_t st) {
+  const size_t smem = sizeof(float) * 2 * kBsNV * kBsCap;
+  static bool configured[2] = {false, false};
+  if (!configured[weighted]) {
+    TK_TRY_CUDA(cudaFuncSetAttribute(weighted ? cone_bp_smem_kernel<true> : cone_bp_smem_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[weighted] = true;
+  }
+  dim3 grid(ceil_div(p.nx, kBsTX), ceil_div(p.ny, kBsTY), ceil_div(p.z_count, kBsZB));
+  if (weighted)
+    cone_bp_smem_kernel<true><<<grid, kBsTX * kBsTY, smem, st>>>(p);
+  else
+    cone_bp_smem_kernel<false><<<grid, kBsTX * kBsTY, smem, st>>>(p);
+  TK_LAUNCHED("cone_bp_smem_kernel");
+  return TK_OK;
+}
 
 static int launch_bp_quad(BpParams p, bool weighted, bool zinv, cudaStream_t st) {
   const long long qview = (long long)(p.band_rows + 1 + kQuadPad) * (p.cols + 1 + kQuadPad);
@@ -1331,6 +1579,43 @@ int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz, doub
                    as_stream(stream), false);
 }
 
+int tk_fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                      void **plan, void *stream) {
+  clear_error();
+  if (!vol || !plan) return fail_arg("tk_fp_plan_create: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1) return fail_arg("tk_fp_plan_create: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0)) return fail_arg("tk_fp_plan_create: spacing must be > 0");
+  FpPlan *pl = new FpPlan();
+  const int rc = fp_plan_create(vol, nz, ny, nx, sz, sy, sx, pl, as_stream(stream));
+  if (rc != TK_OK) {
+    fp_plan_free(pl, as_stream(stream));
+    delete pl;
+    *plan = nullptr;
+    return rc;
+  }
+  *plan = pl;
+  return TK_OK;
+}
+
+int tk_fp_plan_project(void *plan, const double *sources, const double *minv, int n_views, int rows,
+                       int cols, double step, float *out, void *stream) {
+  clear_error();
+  if (!plan || !sources || !minv || !out) return fail_arg("tk_fp_plan_project: null pointer");
+  if (n_views < 1 || rows < 1 || cols < 1 || !(step > 0))
+    return fail_arg("tk_fp_plan_project: bad extent / step");
+  return fp_plan_project(*reinterpret_cast<FpPlan *>(plan), sources, minv, n_views, rows, cols, step,
+                         out, as_stream(stream));
+}
+
+int tk_fp_plan_destroy(void *plan, void *stream) {
+  clear_error();
+  if (!plan) return TK_OK;
+  FpPlan *pl = reinterpret_cast<FpPlan *>(plan);
+  fp_plan_free(pl, as_stream(stream));
+  delete pl;
+  return TK_OK;
+}
+
 int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int cols,
                                const double *sources, const double *minv, int nz, int ny,
                                int nx, double sz, double sy, double sx, double step,
@@ -1389,7 +1674,8 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   dim3 grid(ceil_div(nx, kBpBX), ceil_div(ny, kBpBY), ceil_div(z_count, ZB));
   p.tex = 0;
   BpAlgo algo = bp_algo();
-  if (algo == BpAlgo::kQuad) return launch_bp_quad(p, weighted != 0, zinv, st);
+  if (algo == BpAlgo::kSmem && zinv) return launch_bp_smem(p, weighted != 0, st);
+  if (algo == BpAlgo::kQuad || algo == BpAlgo::kSmem) return launch_bp_quad(p, weighted != 0, zinv, st);
   if (n_views > 2048) algo = BpAlgo::kLdg;  // layered arrays hold <= 2048 layers
   TexLease lease;
   if (algo != BpAlgo::kLdg) {

@@ -92,7 +92,7 @@ __device__ __forceinline__ float preweight(const FilterParams &p, long long row,
 // radix-4 or four radix-2 butterflies (blockDim = N/8), so the register
 // footprint is the same 8 values in every stage.
 template <int R>
-__device__ __forceinline__ void stockham_stage(float2 *x, const float2 *tw, int N, int Ns, int src,
+__device__ __noinline__ void stockham_stage(float2 *x, const float2 *tw, int N, int Ns, int src,
                                                int dst, const FilterParams &p, const float *ia,
                                                const float *ib, long long ra, long long rb,
                                                bool has_b, float *oa, float *ob, const float *wgt) {
@@ -189,7 +189,7 @@ constexpr int filter_threads() {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 2 : 1)) fft_filter_kernel(const FilterParams p) {
+__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 3 : 1)) fft_filter_kernel(const FilterParams p) {
   extern __shared__ float smem[];
   constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);

@@ -17,6 +17,7 @@ module exposes the exact transposes A^T and B^T (``transpose_forward_project``,
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -115,6 +116,57 @@ def fp_tensor(vol: torch.Tensor, geom, step: float, out: torch.Tensor | None = N
                           float(step), _lib.dev_ptr(out), s)
             return out
     raise TypeError(f"unsupported geometry {type(geom).__name__}")
+
+
+class ForwardProjectionPlan:
+    """A cone-beam volume prepared once (tk_fp_plan_create) and projected in
+    view blocks (tk_fp_plan_project) -- used to overlap per-block D2H copies
+    with the next block's kernel.  Use as a context manager; the plan's device
+    memory is released stream-ordered on the creating stream."""
+
+    def __init__(self, vol: torch.Tensor, geom: GeometryCone3D):
+        if not isinstance(geom, GeometryCone3D):
+            raise TypeError("forward projection plans are implemented for cone geometry")
+        vol = _prep(vol, geom.volume_shape, "volume")
+        self.geom, self.device = geom, vol.device
+        self._vol = vol  # keep the source alive until the copies are enqueued
+        self._handle = ctypes.c_void_p()
+        nz, ny, nx = geom.volume_shape
+        sz, sy, sx = geom.volume_spacing
+        with torch.cuda.device(vol.device):
+            self._stream = _lib.stream_ptr(vol.device)
+            _lib.call("tk_fp_plan_create", _lib.dev_ptr(vol), nz, ny, nx, sz, sy, sx,
+                      ctypes.byref(self._handle), self._stream)
+
+    def project(self, views: slice, out: torch.Tensor, step: float) -> torch.Tensor:
+        src, minv = self.geom.ray_constants
+        (src, psrc), (minv, pminv) = _lib.host_f64(src[views]), _lib.host_f64(minv[views])
+        rows, cols = self.geom.detector_shape
+        if tuple(out.shape) != (src.shape[0], rows, cols) or not out.is_contiguous():
+            raise ValueError("plan output must be a contiguous (views, rows, cols) tensor")
+        with torch.cuda.device(self.device):
+            _lib.call("tk_fp_plan_project", self._handle, psrc, pminv, src.shape[0], rows, cols,
+                      float(step), _lib.dev_ptr(out), _lib.stream_ptr(self.device))
+        return out
+
+    def close(self) -> None:
+        if self._handle:
+            with torch.cuda.device(self.device):
+                _lib.call("tk_fp_plan_destroy", self._handle, self._stream)
+            self._handle = ctypes.c_void_p()
+            self._vol = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
 
 def bp_tensor(sino: torch.Tensor, geom, weighted: bool = False,

@@ -395,7 +395,7 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     assert rel(got, want) < TOL
 
 
-@pytest.mark.parametrize("algo", ["quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
 def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     monkeypatch.setenv("TK_BP_ALGO", algo)
     geom = cone(tk, 24, 36, 1.5, 19)
@@ -409,7 +409,7 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
@@ -427,3 +427,39 @@ def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
             r0, r1 = D.row_band(geom, z0, z1)
             slab = bp_cone_tensor_ex(y[:, r0:r1].contiguous(), geom, True, r0, z0, z1 - z0)
             assert rel(slab, full[z0:z1].cpu().numpy()) < 1e-5  # fp32 row-shift rounding
+
+
+@pytest.mark.parametrize("det_pitch", [0.05, 0.4, 3.0])
+def test_bp_smem_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch):
+    """Fine detector pitch makes the CTA footprint exceed the shared-memory tile
+    (global-gather fallback); coarse pitch makes whole volumes fit one tile."""
+    monkeypatch.setenv("TK_BP_ALGO", "smem")
+    geom = tk.circular_cone_geometry((20, 36, 33), (1.0, 0.8, 1.2), (40, 50), (det_pitch, det_pitch), 7,
+                                     2 * np.pi, 1200.0, 750.0)
+    y = np.random.default_rng(23).standard_normal((7, 40, 50))
+    got = tk.back_project(tk.Sinogram(y, (det_pitch, det_pitch)), geom, True).data
+    want = oracle.back_cone_3d(y, geom.matrix_array(), 750.0, (20, 36, 33), (1.0, 0.8, 1.2), True)
+    assert rel(got, want) < TOL
+
+
+def test_overlapped_host_pipeline_matches_device(tk):
+    """Pinned-host boundary calls (chunked plan projection with overlapped D2H,
+    chunked H2D + filtering) equal the device-resident operators bit for bit."""
+    from paper_2511_08427_b200 import ops
+    from paper_2511_08427_b200.filters import fdk_tensor
+    from paper_2511_08427_b200.projectors import ForwardProjectionPlan, fp_tensor
+
+    cfg = {"geometry_kind": "cone3d", "volume_shape": [40, 48, 44], "volume_spacing": [1.0, 1.0, 1.0],
+           "detector_shape": [50, 60], "detector_spacing": [1.4, 1.4], "number_of_projections": 37,
+           "angular_range": 2 * np.pi, "sdd": 1200.0, "sid": 750.0, "filter_kind": "cosine"}
+    geom = ops.PipelineConfig.from_dict(cfg).build_geometry()
+    x = torch.randn(40, 48, 44)
+    want = fp_tensor(x.cuda(), geom, 0.5)
+    got = ops.py_forward_project(x.pin_memory(), cfg)
+    assert got.is_pinned() and torch.equal(got, want.cpu())
+    with ForwardProjectionPlan(x.cuda(), geom) as plan:
+        part = torch.empty(10, 50, 60, device="cuda")
+        plan.project(slice(5, 15), part, 0.5)
+        assert torch.equal(part, want[5:15])
+    rec = ops.py_fbp(got, cfg)
+    assert rec.is_pinned() and torch.allclose(rec, fdk_tensor(want, geom, "cosine").cpu(), rtol=0, atol=1e-6)
