@@ -124,16 +124,20 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+FP_KERNEL = "cone_fp4_kernel"  # the default forward projector (TK_FP_ALGO=ldg4)
+
+
 def ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
-    for p in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
+    """DRAM bytes per launch of the dominant kernel from the newest committed
+    ncu capture of the same configuration (profiles/ncu_*.json)."""
+    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), key=lambda q: q.stat().st_mtime, reverse=True):
         try:
             d = json.loads(p.read_text())
-            k = d.get("cone_fp_kernel") or {}
-            if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
-                return float(k["dram_bytes_per_launch"]), p.name
         except (ValueError, OSError):
             continue
+        k = d.get(FP_KERNEL) or {}
+        if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
+            return float(k["dram_bytes_per_launch"]), f"profiles/{p.name}"
     return None, None
 
 
@@ -365,7 +369,7 @@ def run_ours(args):
             "back_projection": {"ms": round(bp_ms, 3), "gups": round(bp_updates / (bp_ms * 1e-3) / 1e9, 2),
                                 "gather_gbs": round(16.0 * bp_updates / (bp_ms * 1e-3) / 1e9, 1)},
         },
-        "roofline": {"bound": "hbm", "kernel": "cone_fp_kernel", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": FP_KERNEL, "achieved": round(achieved, 1),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",

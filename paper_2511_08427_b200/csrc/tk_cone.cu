@@ -1491,11 +1491,11 @@ enum class BpAlgo { kSmem, kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
-  if (e && !strcmp(e, "quad")) return BpAlgo::kQuad;
+  if (e && !strcmp(e, "smem")) return BpAlgo::kSmem;
   if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
-  return BpAlgo::kSmem;
+  return BpAlgo::kQuad;
 }
 
 constexpr int kBqZB = 16;

@@ -17,6 +17,8 @@
 // stage.  The inverse uses IFFT(y) = conj(FFT(conj(y))) / n.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "tk_common.cuh"
@@ -211,9 +213,132 @@ __global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-row-pair variant: each warp owns one row pair at a time and two
+// private shared buffers (ping-pong), so a Stockham stage reads one buffer and
+// writes the other with only __syncwarp between stages -- no CTA barriers, and
+// every warp progresses independently (latency hidden across warps).
+// Twiddles come from the global table through L1.
+// ---------------------------------------------------------------------------
+constexpr int kFwWarps = 4;
+
+template <int R>
+__device__ __forceinline__ void warp_stage(const float2 *__restrict__ xin, float2 *__restrict__ xout,
+                                           const float2 *__restrict__ tw, int N, int Ns, int src,
+                                           int dst, const FilterParams &p, const float *ia,
+                                           const float *ib, long long ra, long long rb, bool has_b,
+                                           float *oa, float *ob, const float *__restrict__ wgt) {
+  const int lane = threadIdx.x & 31;
+  const int nb = N / R;
+  const int tstride = N / (Ns * R);
+  for (int j = lane; j < nb; j += 32) {
+    const int k = j % Ns;
+    float2 v[8];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = j + r * nb;
+      float2 z;
+      if (src == 1) {
+        float a = 0.f, b = 0.f;
+        if (e < p.width) {
+          a = __ldg(ia + e) * preweight(p, ra, e);
+          if (has_b) b = __ldg(ib + e) * preweight(p, rb, e);
+        }
+        z = make_float2(a, b);
+      } else {
+        z = xin[e];
+        if (src == 2) {
+          const float w = __ldg(wgt + (e <= N / 2 ? e : N - e));
+          z = make_float2(z.x * w, -z.y * w);
+        }
+      }
+      v[r] = (r > 0 && Ns > 1) ? cmul(z, __ldg(tw + r * k * tstride)) : z;
+    }
+    if (R == 8) dft8(v);
+    if (R == 4) dft4(v[0], v[1], v[2], v[3]);
+    if (R == 2) dft2(v);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int o = base + r * Ns;
+      if (dst == 1) {
+        if (o < p.width) {
+          oa[o] = v[r].x;
+          if (has_b) ob[o] = -v[r].y;
+        }
+      } else {
+        xout[o] = v[r];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int LOGN, bool INV, int S>
+__device__ __forceinline__ void warp_pass(float2 *bufA, float2 *bufB, const float2 *tw,
+                                          const FilterParams &p, const float *ia, const float *ib,
+                                          long long ra, long long rb, bool has_b, float *oa,
+                                          float *ob, const float *wgt) {
+  using P = FftPlan<LOGN>;
+  if constexpr (S < P::kStages) {
+    constexpr int src = S == 0 ? (INV ? 2 : 1) : 0;
+    constexpr int dst = (INV && S == P::kStages - 1) ? 1 : 0;
+    // stage S reads buffer (S odd ? B : A) and writes the other; the forward
+    // pass leaves its result in buffer (kStages odd ? B : A) = the inverse input
+    constexpr bool flip = INV && (P::kStages % 2 == 1);
+    constexpr bool read_b = ((S % 2) == 1) != flip;
+    warp_stage<P::radix(S)>(read_b ? bufB : bufA, read_b ? bufA : bufB, tw, P::kN, P::span(S), src,
+                            dst, p, ia, ib, ra, rb, has_b, oa, ob, wgt);
+    warp_pass<LOGN, INV, S + 1>(bufA, bufB, tw, p, ia, ib, ra, rb, has_b, oa, ob, wgt);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(32 * kFwWarps) fft_filter_warp_kernel(const FilterParams p) {
+  extern __shared__ float smem[];
+  constexpr int N = 1 << LOGN;
+  const int warp = threadIdx.x >> 5;
+  float2 *bufA = reinterpret_cast<float2 *>(smem) + (size_t)warp * 2 * N;
+  float2 *bufB = bufA + N;
+  const long long n_pairs = (p.n_rows + 1) / 2;
+  for (long long pair = (long long)blockIdx.x * kFwWarps + warp; pair < n_pairs;
+       pair += (long long)gridDim.x * kFwWarps) {
+    const long long ra = 2 * pair, rb = ra + 1;
+    const bool has_b = rb < p.n_rows;
+    const float *ia = p.in + ra * p.width;
+    const float *ib = p.in + rb * p.width;
+    float *oa = p.out + ra * p.width;
+    float *ob = p.out + rb * p.width;
+    // forward: stage 0 reads global and writes A (buffer names per warp_pass)
+    warp_pass<LOGN, false, 0>(bufB, bufA, p.tw, p, ia, ib, ra, rb, has_b, oa, ob, p.wgt);
+    warp_pass<LOGN, true, 0>(bufB, bufA, p.tw, p, ia, ib, ra, rb, has_b, oa, ob, p.wgt);
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_filter_warp(const FilterParams &p, cudaStream_t st) {
+  constexpr int N = 1 << LOGN;
+  const size_t smem = sizeof(float2) * 2 * N * kFwWarps;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fft_filter_warp_kernel<LOGN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const long long pairs = (p.n_rows + 1) / 2;
+  const int per_sm = std::max(1, (int)((220 * 1024) / smem));
+  const long long want = (pairs + kFwWarps - 1) / kFwWarps;
+  const unsigned grid = (unsigned)std::min<long long>(want, (long long)sm_count() * per_sm);
+  fft_filter_warp_kernel<LOGN><<<grid, 32 * kFwWarps, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 static cudaError_t launch_filter(const FilterParams &p, size_t smem, cudaStream_t st) {
   constexpr int N = 1 << LOGN;
+  if (LOGN <= 11) {  // warp variant unless TK_FILTER_ALGO=cta (2 x 16 KB per warp at N = 2048)
+    const char *e = getenv("TK_FILTER_ALGO");
+    if (!(e && !strcmp(e, "cta"))) return launch_filter_warp<LOGN>(p, st);
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fft_filter_kernel<LOGN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
