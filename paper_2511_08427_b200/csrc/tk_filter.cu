@@ -335,9 +335,9 @@ static cudaError_t launch_filter_warp(const FilterParams &p, cudaStream_t st) {
 template <int LOGN>
 static cudaError_t launch_filter(const FilterParams &p, size_t smem, cudaStream_t st) {
   constexpr int N = 1 << LOGN;
-  if (LOGN <= 11) {  // warp variant unless TK_FILTER_ALGO=cta (2 x 16 KB per warp at N = 2048)
+  if (LOGN <= 11) {  // TK_FILTER_ALGO=warp: warp-per-row-pair variant (measured slower at cfg4)
     const char *e = getenv("TK_FILTER_ALGO");
-    if (!(e && !strcmp(e, "cta"))) return launch_filter_warp<LOGN>(p, st);
+    if (e && !strcmp(e, "warp")) return launch_filter_warp<LOGN>(p, st);
   }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fft_filter_kernel<LOGN>,

@@ -33,7 +33,7 @@ void tex_release(TexLease &lease, cudaStream_t st);
 __device__ __forceinline__ float4 gather_a2d(cudaTextureObject_t t, int layer, float x_center,
                                              float y_center) {
   float4 r;
-  asm volatile("tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
+  asm("tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(t), "r"(layer), "f"(x_center), "f"(y_center));
   return r;
