@@ -120,7 +120,7 @@ __device__ __noinline__ void stockham_stage(float2 *x, const float2 *tw, int N, 
           }
           z = make_float2(a, b);
         } else {
-          z = x[e];
+          z = x[e + (e >> 4)];  // one float2 of padding per 16: conflict-free strides
           if (src == 2) {
             const float w = wgt[e <= N / 2 ? e : N - e];
             z = make_float2(z.x * w, -z.y * w);
@@ -149,7 +149,7 @@ __device__ __noinline__ void stockham_stage(float2 *x, const float2 *tw, int N, 
             if (has_b) ob[o] = -v[c * R + r].y;
           }
         } else {
-          x[o] = v[c * R + r];
+          x[o + (o >> 4)] = v[c * R + r];
         }
       }
     }
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>(
   extern __shared__ float smem[];
   constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);
-  float2 *tw = x + N;
+  float2 *tw = x + N + N / 16;
   float *wgt = reinterpret_cast<float *>(tw + N);
   for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = p.tw[i];
   for (int i = threadIdx.x; i <= N / 2; i += blockDim.x) wgt[i] = p.wgt[i];
@@ -395,7 +395,7 @@ extern "C" int tk_fft_filter_rows_ex(const float *in, long long n_rows, int widt
   p.sdd = (float)sdd;
   p.du = (float)du;
   p.dv = (float)dv;
-  const size_t smem = sizeof(float2) * 2 * n_pad + sizeof(float) * (n_pad / 2 + 1);
+  const size_t smem = sizeof(float2) * (2 * n_pad + n_pad / 16) + sizeof(float) * (n_pad / 2 + 1);
   int lg = 0;
   while ((1 << lg) < n_pad) ++lg;
   cudaError_t e;

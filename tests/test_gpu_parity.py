@@ -463,3 +463,67 @@ def test_overlapped_host_pipeline_matches_device(tk):
         assert torch.equal(part, want[5:15])
     rec = ops.py_fbp(got, cfg)
     assert rec.is_pinned() and torch.allclose(rec, fdk_tensor(want, geom, "cosine").cpu(), rtol=0, atol=1e-6)
+
+
+def test_grid_files_roundtrip_and_reference_format(tk, tmp_path, golden):
+    """Grid pairs written here read back bit-exactly and carry the reference's
+    header schema (grids.py:122-212)."""
+    import json
+
+    x = golden("cone3d")["x"]
+    v = tk.Volume(x, (1.0, 1.0, 1.0))
+    tk.write_grid(v, tmp_path / "vol")
+    hdr = json.loads((tmp_path / "vol.json").read_text())
+    assert hdr == {"kind": "volume", "shape": [16, 16, 16], "spacing": [1.0, 1.0, 1.0], "dtype": "f32le",
+                   "order": "C"}
+    back = tk.read_grid(tmp_path / "vol.raw")
+    assert torch.equal(back.data, v.data)
+    s = tk.Sinogram(golden("cone3d")["y"], (1.6, 1.6))
+    tk.write_grid(s, tmp_path / "sino.json")
+    s2 = tk.read_grid(tmp_path / "sino")
+    assert isinstance(s2, tk.Sinogram) and s2.detector_spacing == (1.6, 1.6) and torch.equal(s2.data, s.data)
+    with pytest.raises(tk.SizeMismatchError):
+        (tmp_path / "bad.json").write_text((tmp_path / "vol.json").read_text())
+        (tmp_path / "bad.raw").write_bytes(b"\0" * 12)
+        tk.read_grid(tmp_path / "bad")
+
+
+def test_2d_layers_autograd(tk):
+    ang = tk.circular_trajectory_2d(60, 2 * np.pi)
+    gp = tk.GeometryParallel2D((24, 24), (1, 1), 36, 1.0, ang)
+    gf = tk.GeometryFan2D((24, 24), (1, 1), 40, 1.5, ang, sdd=1200.0, sid=750.0)
+    for fwd, bwd, g in ((tk.ParallelProjection2D, tk.ParallelBackProjection2D, gp),
+                        (tk.FanProjection2D, tk.FanBackProjection2D, gf)):
+        x = torch.randn(24, 24, device="cuda", requires_grad=True)
+        y = torch.randn(*g.sinogram_shape, device="cuda")
+        (fwd.apply(x, g) * y).sum().backward()
+        assert torch.equal(x.grad, tk.back_project(tk.Sinogram(y, (g.detector_spacing,)), g).data)
+        x2 = torch.randn(24, 24, device="cuda", requires_grad=True)
+        (fwd.apply(x2, g, "matched") * y).sum().backward()
+        want = tk.transpose_forward_project(tk.Sinogram(y, (g.detector_spacing,)), g).data
+        assert rel(x2.grad, want.cpu().numpy()) < 1e-5
+        s = torch.randn(*g.sinogram_shape, device="cuda", requires_grad=True)
+        xx = torch.randn(24, 24, device="cuda")
+        (bwd.apply(s, g) * xx).sum().backward()
+        assert torch.equal(s.grad, tk.forward_project(tk.Volume(xx, (1, 1)), g).data)
+
+
+def test_helical_learned_reconstruction_gradient_step(tk):
+    """cfg5 pattern at small scale: loss 1/2 |A x - y|^2 on a helical orbit,
+    gradient through ConeProjection3D (paired and matched), one descent step
+    lowers the loss."""
+    mats = tk.helical_trajectory_3d(48, 4 * np.pi, 1200.0, 750.0, (40, 40), (1.2, 1.2), -8.0, 8.0)
+    geom = tk.GeometryCone3D((32, 32, 32), (1, 1, 1), (40, 40), (1.2, 1.2), mats, 1200.0, 750.0)
+    truth = tk.phantoms.shepp_logan_3d((32, 32, 32))
+    y = tk.ConeProjection3D.apply(truth, geom) + 0.01 * torch.randn(48, 40, 40, device="cuda")
+    for adjoint in ("paired", "matched"):
+        x = torch.zeros(32, 32, 32, device="cuda", requires_grad=True)
+        loss = 0.5 * ((tk.ConeProjection3D.apply(x, geom, adjoint) - y) ** 2).sum()
+        loss.backward()
+        with torch.no_grad():
+            g = x.grad
+            ag = tk.ConeProjection3D.apply(g, geom)
+            t = float((g * g).sum() / (ag * ag).sum())  # exact line search for the matched gradient
+            x2 = x - t * g
+            loss2 = 0.5 * ((tk.ConeProjection3D.apply(x2, geom) - y) ** 2).sum()
+        assert float(loss2) < float(loss)
