@@ -191,7 +191,7 @@ constexpr int filter_threads() {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 3 : 1)) fft_filter_kernel(const FilterParams p) {
+__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 4 : 1)) fft_filter_kernel(const FilterParams p) {
   extern __shared__ float smem[];
   constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);
