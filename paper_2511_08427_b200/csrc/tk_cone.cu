@@ -934,121 +934,6 @@ __global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_quad_kernel(const BpP
 }
 
 // ---------------------------------------------------------------------------
-// Row-walk back projector ("pairs", default for z-invariant trajectories whose
-// detector rows advance with z).
-//
-// The sinogram is rewritten as column pairs
-//   D[v][r+2][c+2] = (S[r][c], S[r][c+1]),  r in [-2, R], c in [-2, C]
-// (zero outside the detector).  Along a thread's z-run the column is fixed and
-// the row coordinate advances by dr = 1.1..1.8 rows per voxel, so consecutive
-// voxels share detector rows: each thread walks down the rows keeping the two
-// current pairs in registers and loads only the rows it has not seen --
-// ~dr pair loads (8 B each) per update instead of one 16-byte quad, which is
-// what the L1 load path (the quad kernel's bound) has to deliver.
-// ---------------------------------------------------------------------------
-__global__ void pairify_kernel(const float *__restrict__ sino, int n_views, int rows, int cols,
-                               float2 *__restrict__ pairs) {
-  // rows r in [-2, R+1] (the walk's lower pair of row R is row R+1), cols c in [-2, C]
-  const int qc = cols + 1 + kQuadPad, qr = rows + 2 + kQuadPad;
-  const long long total = (long long)n_views * qr * qc;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % qc) - kQuadPad;
-    const long long t = i / qc;
-    const int r0 = (int)(t % qr) - kQuadPad;
-    const int v = (int)(t / qr);
-    const float *s = sino + ((long long)v * rows + r0) * cols;
-    const bool ra = (unsigned)r0 < (unsigned)rows;
-    const float a = (ra && (unsigned)c0 < (unsigned)cols) ? __ldg(s + c0) : 0.f;
-    const float b = (ra && (unsigned)(c0 + 1) < (unsigned)cols) ? __ldg(s + c0 + 1) : 0.f;
-    pairs[i] = make_float2(a, b);
-  }
-}
-
-template <int ZB, bool WEIGHTED>
-__global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_pairs_kernel(const BpParams p,
-                                                                       const float2 *__restrict__ pairs) {
-  __shared__ ConeVoxView sv[kBpChunk];
-  const int ix = blockIdx.x * kBqBX + threadIdx.x;
-  const int iy = blockIdx.y * kBqBY + threadIdx.y;
-  const int zl0 = blockIdx.z * ZB;
-  const bool active = ix < p.nx && iy < p.ny;
-  const float xc = (float)ix - p.cx;
-  const float yc = (float)iy - p.cy;
-  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
-  const int tid = threadIdx.y * kBqBX + threadIdx.x;
-  const int qc = p.cols + 1 + kQuadPad;
-  const int rmax = p.band_rows;
-  const long long qview = (long long)(p.band_rows + 2 + kQuadPad) * qc;
-  const float colmax = (float)(p.cols - 1);
-
-  float acc[ZB];
-#pragma unroll
-  for (int k = 0; k < ZB; ++k) acc[k] = 0.f;
-
-  for (int v0 = 0; v0 < p.n_views; v0 += kBpChunk) {
-    const int nch = min(kBpChunk, p.n_views - v0);
-    __syncthreads();
-    for (int i = tid; i < nch * 12; i += kBqBX * kBqBY)
-      reinterpret_cast<float *>(sv)[i] = __ldg(reinterpret_cast<const float *>(p.views + v0) + i);
-    __syncthreads();
-    if (!active) continue;
-    for (int j = 0; j < nch; ++j) {
-      const ConeVoxView &V = sv[j];
-      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
-      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
-      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
-      if (!(w0 > (float)kTiny)) continue;  // _kernels.py:297-298
-      const float rw = 1.f / w0;
-      const float fc = fmaf(a0, rw, p.cu);
-      const float flc = floorf(fc);
-      if (!(flc >= -1.f && flc <= colmax)) continue;  // both column taps off the detector
-      const float wc = fc - flc;
-      float q = 1.f;
-      if (WEIGHTED) {
-        q = p.sid * rw;
-        q *= q;
-      }
-      const float g0 = q * (1.f - wc), g1 = q * wc;
-      // pairs of this column; row index r lives at col + (r + 2) * qc
-      const float2 *col = pairs + (long long)(v0 + j) * qview + ((int)flc + kQuadPad) +
-                          (long long)kQuadPad * qc;
-      const float fr0 = fmaf(b0, rw, p.cv);
-      const float dr = V.b[2] * rw;  // >= 0 (host-checked)
-      int cur = min(max(__float2int_rd(fr0), -kQuadPad), rmax);
-      float2 top = __ldg(col + cur * qc), bot = __ldg(col + (cur + 1) * qc);
-#pragma unroll
-      for (int k = 0; k < ZB; ++k) {
-        const float fr = fmaf((float)k, dr, fr0);
-        const float flr = floorf(fr);
-        const int rk = min(max((int)flr, -kQuadPad), rmax);
-        const int d = rk - cur;
-        if (d == 1) {
-          top = bot;
-          bot = __ldg(col + (rk + 1) * qc);
-        } else if (d != 0) {
-          top = __ldg(col + rk * qc);
-          bot = __ldg(col + (rk + 1) * qc);
-        }
-        cur = rk;
-        const float tr = fmaf(g1, top.y, g0 * top.x);
-        const float br = fmaf(g1, bot.y, g0 * bot.x);
-        acc[k] += fmaf(fr - flr, br - tr, tr);
-      }
-    }
-  }
-  if (!active) return;
-#pragma unroll
-  for (int k = 0; k < ZB; ++k) {
-    const int zl = zl0 + k;
-    if (zl < p.z_count) {
-      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
-      *o = p.accumulate ? *o + acc[k] : acc[k];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Shared-memory staged back projector ("smem", default for z-invariant
 // trajectories) -- the north star's "detector tiles for a batch of views are
 // staged into shared memory".
@@ -1605,16 +1490,15 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
 }
 
 // Back-projector algorithm: TK_BP_ALGO = ldg (default) | tex | hwtex.
-enum class BpAlgo { kPairs, kSmem, kQuad, kLdg, kTex, kHwTex };
+enum class BpAlgo { kSmem, kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
-  if (e && !strcmp(e, "quad")) return BpAlgo::kQuad;
   if (e && !strcmp(e, "smem")) return BpAlgo::kSmem;
   if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
-  return BpAlgo::kPairs;
+  return BpAlgo::kQuad;
 }
 
 constexpr int kBqZB = 16;
@@ -1633,24 +1517,6 @@ static int launch_bp_smem(const BpParams &p, bool weighted, cudaStream_t st) {
   else
     cone_bp_smem_kernel<false><<<grid, kBsTX * kBsTY, smem, st>>>(p);
   TK_LAUNCHED("cone_bp_smem_kernel");
-  return TK_OK;
-}
-
-static int launch_bp_pairs(const BpParams &p, bool weighted, cudaStream_t st) {
-  const long long qview = (long long)(p.band_rows + 2 + kQuadPad) * (p.cols + 1 + kQuadPad);
-  const long long nq = qview * p.n_views;
-  Scratch pairs;
-  TK_TRY_CUDA(pairs.alloc(sizeof(float2) * nq, st));
-  const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(nq, 256), (long long)sm_count() * 32);
-  pairify_kernel<<<qgrid, 256, 0, st>>>(p.sino, p.n_views, p.band_rows, p.cols, pairs.as<float2>());
-  TK_LAUNCHED("pairify_kernel");
-  dim3 block(kBqBX, kBqBY);
-  dim3 grid(ceil_div(p.nx, kBqBX), ceil_div(p.ny, kBqBY), ceil_div(p.z_count, kBqZB));
-  if (weighted)
-    cone_bp_pairs_kernel<kBqZB, true><<<grid, block, 0, st>>>(p, pairs.as<float2>());
-  else
-    cone_bp_pairs_kernel<kBqZB, false><<<grid, block, 0, st>>>(p, pairs.as<float2>());
-  TK_LAUNCHED("cone_bp_pairs_kernel");
   return TK_OK;
 }
 
@@ -1785,8 +1651,6 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   std::vector<ConeVoxView> hv;
   bool zinv = true;
   pack_bp_views(mats, n_views, sx, sy, sz, cu, cv, hv, zinv);
-  bool rows_advance = true;  // detector row coordinate non-decreasing in z (row walk)
-  for (const ConeVoxView &V : hv) rows_advance &= V.b[2] >= 0.f;
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeVoxView) * n_views, st));
   BpParams p;
@@ -1813,10 +1677,8 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   dim3 grid(ceil_div(nx, kBpBX), ceil_div(ny, kBpBY), ceil_div(z_count, ZB));
   p.tex = 0;
   BpAlgo algo = bp_algo();
-  if (algo == BpAlgo::kPairs && zinv && rows_advance) return launch_bp_pairs(p, weighted != 0, st);
   if (algo == BpAlgo::kSmem && zinv) return launch_bp_smem(p, weighted != 0, st);
-  if (algo == BpAlgo::kQuad || algo == BpAlgo::kSmem || algo == BpAlgo::kPairs)
-    return launch_bp_quad(p, weighted != 0, zinv, st);
+  if (algo == BpAlgo::kQuad || algo == BpAlgo::kSmem) return launch_bp_quad(p, weighted != 0, zinv, st);
   if (n_views > 2048) algo = BpAlgo::kLdg;  // layered arrays hold <= 2048 layers
   TexLease lease;
   if (algo != BpAlgo::kLdg) {

@@ -83,7 +83,7 @@ __device__ __forceinline__ float preweight(const FilterParams &p, long long row,
   const int r = (int)(row % p.band_rows) + p.row_offset;
   const float u = ((float)i - 0.5f * (float)(p.width - 1)) * p.du;
   const float v = ((float)r - 0.5f * (float)(p.det_rows - 1)) * p.dv;
-  return p.sdd / sqrtf(fmaf(p.sdd, p.sdd, fmaf(u, u, v * v)));
+  return p.sdd * rsqrtf(fmaf(p.sdd, p.sdd, fmaf(u, u, v * v)));  // ~2 ulp, well inside 1e-4
 }
 
 // Source of stage inputs: 0 = shared buffer, 1 = global rows (first forward
@@ -107,7 +107,7 @@ __device__ __noinline__ void stockham_stage(float2 *x, const float2 *tw, int N, 
 #pragma unroll
     for (int c = 0; c < kB; ++c) {
       const int j = threadIdx.x * kB + c;
-      const int k = j % Ns;
+      const int k = j & (Ns - 1);  // Ns is a power of two
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int e = j + r * nb;
@@ -138,8 +138,8 @@ __device__ __noinline__ void stockham_stage(float2 *x, const float2 *tw, int N, 
 #pragma unroll
     for (int c = 0; c < kB; ++c) {
       const int j = threadIdx.x * kB + c;
-      const int k = j % Ns;
-      const int base = (j / Ns) * Ns * R + k;
+      const int k = j & (Ns - 1);  // Ns is a power of two
+      const int base = (j - k) * R + k;  // (j / Ns) * Ns * R + k
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int o = base + r * Ns;
@@ -191,7 +191,7 @@ constexpr int filter_threads() {
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 4 : 1)) fft_filter_kernel(const FilterParams p) {
+__global__ void __launch_bounds__(filter_threads<LOGN>(), (filter_threads<LOGN>() <= 256 ? 3 : 1)) fft_filter_kernel(const FilterParams p) {
   extern __shared__ float smem[];
   constexpr int N = 1 << LOGN;
   float2 *x = reinterpret_cast<float2 *>(smem);
@@ -232,7 +232,7 @@ __device__ __forceinline__ void warp_stage(const float2 *__restrict__ xin, float
   const int nb = N / R;
   const int tstride = N / (Ns * R);
   for (int j = lane; j < nb; j += 32) {
-    const int k = j % Ns;
+    const int k = j & (Ns - 1);  // Ns is a power of two
     float2 v[8];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -257,7 +257,7 @@ __device__ __forceinline__ void warp_stage(const float2 *__restrict__ xin, float
     if (R == 8) dft8(v);
     if (R == 4) dft4(v[0], v[1], v[2], v[3]);
     if (R == 2) dft2(v);
-    const int base = (j / Ns) * Ns * R + k;
+    const int base = (j - k) * R + k;  // (j / Ns) * Ns * R + k
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int o = base + r * Ns;

@@ -395,7 +395,7 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     assert rel(got, want) < TOL
 
 
-@pytest.mark.parametrize("algo", ["pairs", "smem", "quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
 def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     monkeypatch.setenv("TK_BP_ALGO", algo)
     geom = cone(tk, 24, 36, 1.5, 19)
@@ -409,7 +409,7 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["pairs", "smem", "quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
