@@ -1366,8 +1366,8 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   dim3 block(kFp2BX, kFp2BY);
   const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
   if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-  const char *mb = getenv("TK_FP2_MINB");
-  const int minb = mb ? atoi(mb) : 10;
+  const char *mb = getenv("TK_FP2_MINB");  // 10 or 12 resident CTAs per SM
+  const int minb = mb ? atoi(mb) : 12;  // 12 CTAs x 128 threads (<= 40 regs): measured best
   auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
   kern<<<(unsigned)nblocks, block, 0, st>>>(pl.qA, pl.qB, pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
                                             dviews.as<Fp2View>(), rows, cols, n_views, step, out);
