@@ -424,6 +424,131 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
   *dst = acc * (float)step;
 }
 
+// ---------------------------------------------------------------------------
+// Forward projection, coefficient-cell variant ("ldg8", default).
+//
+// The ncu capture of cone_fp4_kernel (profiles/ncu_r01c_*) shows an issue-
+// bound loop of ~42 instructions per sample, 5 of them conversions (3 FRND
+// + 2 F2I, quarter-rate pipe).  Here
+//   * every margin-padded cell (z, b, a) stores the 8 coefficients of its
+//     trilinear polynomial in Horner order, 32 B aligned, so a cell is ONE
+//     256-bit load (one sector) and the interpolation is 7 FFMA:
+//       f = c000 + wa c100 + wb c010 + wa wb c110
+//         + wz (c001 + wa c101 + wb c011 + wa wb c111);
+//   * floor() is an FADD.RM with 1.5 * 2^23 (the sum's mantissa IS the
+//     integer), so the loop has no conversion instructions: the cell index is
+//     formed from the raw float bits with two IMADs, the fraction fa - floor(fa)
+//     is exact as before.
+// Traversal, sample positions and loop counts are those of cone_fp2_kernel.
+// ---------------------------------------------------------------------------
+struct __align__(32) Cell8 {
+  float c[8];  // c000 c100 c010 c110 | c001 c101 c011 c111   (a fastest, then b, then z)
+};
+
+__global__ void coef_volume_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
+                                   Cell8 *__restrict__ q) {
+  constexpr int m = kFpMargin;
+  const int na = swap_xy ? ny : nx, nb = swap_xy ? nx : ny;
+  const int pa = na + 2 * m, pb = nb + 2 * m, pz = nz + 2 * m;
+  const long long total = (long long)pz * pb * pa;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(i % pa) - m;
+    const long long t = i / pa;
+    const int b = (int)(t % pb) - m;
+    const int z = (int)(t / pb) - m;
+    float v[8];  // v[dz*4 + db*2 + da]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int aa = a + (j & 1), bb = b + ((j >> 1) & 1), zz = z + (j >> 2);
+      float val = 0.f;
+      if ((unsigned)zz < (unsigned)nz && (unsigned)aa < (unsigned)na && (unsigned)bb < (unsigned)nb) {
+        const int x = swap_xy ? bb : aa, y = swap_xy ? aa : bb;
+        val = __ldg(vol + ((long long)zz * ny + y) * nx + x);
+      }
+      v[j] = val;
+    }
+    Cell8 c;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // z = 0 / 1 slice: bilinear coefficients
+      const float *s = v + 4 * h;
+      c.c[4 * h + 0] = s[0];
+      c.c[4 * h + 1] = s[1] - s[0];
+      c.c[4 * h + 2] = s[2] - s[0];
+      c.c[4 * h + 3] = (s[3] - s[2]) - (s[1] - s[0]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c.c[4 + j] -= c.c[j];  // z differences
+    q[i] = c;
+  }
+}
+
+__device__ __forceinline__ void ldg_cell8(const Cell8 *p, float (&c)[8]) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(c[0]), "=f"(c[1]), "=f"(c[2]), "=f"(c[3]), "=f"(c[4]), "=f"(c[5]), "=f"(c[6]),
+                 "=f"(c[7])
+               : "l"(p));
+}
+
+constexpr float kFloorMagic = 12582912.f;  // 1.5 * 2^23: x + M rounded down = M + floor(x)
+constexpr unsigned kFloorBits = 0x4B400000u;
+
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
+    cone_fp8_kernel(const Cell8 *__restrict__ qA, const Cell8 *__restrict__ qB, int nx, int ny,
+                    int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
+                    int rows, int cols, int n_views, double step, float *__restrict__ out) {
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r = rb * kFp2BY + threadIdx.y;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  const Cell8 *q = W.swap ? qB : qA;
+  const int na = W.swap ? ny : nx, nb = W.swap ? nx : ny;
+  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const unsigned pa = (unsigned)(na + 2 * kFpMargin);
+  const unsigned ps = (unsigned)(nb + 2 * kFpMargin) * pa;
+  // raw index = bits(za) * ps + bits(zb) * pa + bits(xa) = cell + bias  (mod 2^32)
+  const unsigned bias = kFloorBits * (1u + pa + ps);
+  unsigned cell = ~0u;
+  float k8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto sample = [&](float kk) -> float {
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float xa = __fadd_rd(fa, kFloorMagic), xb = __fadd_rd(fb, kFloorMagic),
+                xz = __fadd_rd(fz, kFloorMagic);
+    const unsigned id = __float_as_uint(xz) * ps + (__float_as_uint(xb) * pa + __float_as_uint(xa));
+    if (id != cell) {
+      cell = id;
+      ldg_cell8(q + (id - bias), k8);
+    }
+    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float lo = fmaf(wb, fmaf(wa, k8[3], k8[2]), fmaf(wa, k8[1], k8[0]));
+    const float dz = fmaf(wb, fmaf(wa, k8[7], k8[6]), fmaf(wa, k8[5], k8[4]));
+    return fmaf(wz, dz, lo);
+  };
+  float acc = 0.f;
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+#pragma unroll 4
+  for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+  acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
+  *dst = acc * (float)step;
+}
+
 // Two rays per thread (detector rows r and r+1 of the same column): the two
 // independent sample chains double the loads in flight per warp, hiding L1/L2
 // latency without more resident warps.  Same arithmetic as cone_fp2_kernel.
@@ -1303,25 +1428,28 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg4 (default) | ldg2 | ldg | tex | hwtex.
-enum class FpAlgo { kLdg4, kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg8 (default) | ldg4 | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg8, kLdg4, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
+  if (e && !strcmp(e, "ldg4")) return FpAlgo::kLdg4;
   if (e && !strcmp(e, "ldg")) return FpAlgo::kLdg;
   if (e && !strcmp(e, "ldg2")) return FpAlgo::kLdg2;
   if (e && !strcmp(e, "tex")) return FpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
-  return FpAlgo::kLdg4;
+  return FpAlgo::kLdg8;
 }
 
-// A forward-projection plan: the two quad-tap orientation copies of one
-// volume, built once and reused by any number of view blocks (the e2e path
-// projects view chunks so their D2H copies overlap the next chunk's kernel).
+// A forward-projection plan: the two orientation copies of one volume (8-
+// coefficient cells for ldg8, tap quads for ldg4), built once and reused by
+// any number of view blocks (the e2e path projects view chunks so their D2H
+// copies overlap the next chunk's kernel).
 struct FpPlan {
   int nz, ny, nx;
   double sz, sy, sx;
-  float4 *qA = nullptr, *qB = nullptr;
+  bool coef = true;  // Cell8 (ldg8) or float4 quads (ldg4)
+  void *qA = nullptr, *qB = nullptr;
 };
 
 static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
@@ -1332,15 +1460,23 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->sz = sz;
   plan->sy = sy;
   plan->sx = sx;
+  plan->coef = fp_algo() != FpAlgo::kLdg4;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
-  TK_TRY_CUDA(cudaMallocAsync(&plan->qA, sizeof(float4) * ncell, st));
-  TK_TRY_CUDA(cudaMallocAsync(&plan->qB, sizeof(float4) * ncell, st));
-  quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, plan->qA);
-  TK_LAUNCHED("quad_volume_kernel");
-  quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 1, plan->qB);
-  TK_LAUNCHED("quad_volume_kernel");
+  const size_t esz = plan->coef ? sizeof(Cell8) : sizeof(float4);
+  TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * ncell, st));
+  TK_TRY_CUDA(cudaMallocAsync(&plan->qB, esz * ncell, st));
+  for (int sw = 0; sw < 2; ++sw) {
+    void *dst = sw ? plan->qB : plan->qA;
+    if (plan->coef) {
+      coef_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<Cell8 *>(dst));
+      TK_LAUNCHED("coef_volume_kernel");
+    } else {
+      quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst));
+      TK_LAUNCHED("quad_volume_kernel");
+    }
+  }
   return TK_OK;
 }
 
@@ -1366,12 +1502,21 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   dim3 block(kFp2BX, kFp2BY);
   const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
   if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-  const char *mb = getenv("TK_FP2_MINB");  // 10 or 12 resident CTAs per SM
-  const int minb = mb ? atoi(mb) : 12;  // 12 CTAs x 128 threads (<= 40 regs): measured best
-  auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
-  kern<<<(unsigned)nblocks, block, 0, st>>>(pl.qA, pl.qB, pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
-                                            dviews.as<Fp2View>(), rows, cols, n_views, step, out);
-  TK_LAUNCHED("cone_fp4_kernel");
+  const char *mb = getenv("TK_FP2_MINB");  // 8, 10 or 12 resident CTAs per SM
+  const int minb = mb ? atoi(mb) : 12;  // 12 CTAs x 128 threads (<= 40 regs): measured best for ldg4
+  if (pl.coef) {
+    auto kern = minb >= 12 ? cone_fp8_kernel<12> : (minb >= 10 ? cone_fp8_kernel<10> : cone_fp8_kernel<8>);
+    kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const Cell8 *>(pl.qA), static_cast<const Cell8 *>(pl.qB),
+                                              pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
+                                              cols, n_views, step, out);
+    TK_LAUNCHED("cone_fp8_kernel");
+  } else {
+    auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
+    kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const float4 *>(pl.qA), static_cast<const float4 *>(pl.qB),
+                                              pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
+                                              cols, n_views, step, out);
+    TK_LAUNCHED("cone_fp4_kernel");
+  }
   return TK_OK;
 }
 
@@ -1446,7 +1591,7 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
-  if (!adjoint && algo == FpAlgo::kLdg4)
+  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4))
     return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);

@@ -28,6 +28,13 @@ METRICS = {
     "launch__registers_per_thread": "registers",
     "sm__inst_executed_pipe_tex.avg.pct_of_peak_sustained_active": "tex_pipe_pct",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_pipe_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "lds_wavefronts",
+    "l1tex__t_bytes.sum.per_second": "l1tex_bytes_per_s",
+    "lts__t_bytes.sum.per_second": "lts_bytes_per_s",
 }
 SCALE = {"duration": ("ms", {"s": 1e3, "ms": 1.0, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6, "ns": 1e-6}),
          "dram_read": ("bytes", {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}),
