@@ -124,7 +124,8 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-FP_KERNEL = "cone_fp4_kernel"  # the default forward projector (TK_FP_ALGO=ldg4)
+FP_KERNEL = "cone_fp4_kernel"  # the default forward projector (TK_FP_ALGO=ldg4m: <.., true>)
+BP_KERNEL = "cone_bp_quad_kernel"  # the default back projector (TK_BP_ALGO=quad)
 
 
 def ncu_traffic():
@@ -139,6 +140,28 @@ def ncu_traffic():
         if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
             return float(k["dram_bytes_per_launch"]), f"profiles/{p.name}"
     return None, None
+
+
+def gather_roofline(fp_bytes, fp_ms, bp_bytes, bp_ms, clocks):
+    """Both projectors are gather-bound: their ceiling is the L1 load data path
+    (LSU writeback, 128 B/clk/SM; ncu derived__l1tex__lsu_writeback_bytes
+    peak_sustained = 128 x 148 B/cycle), not HBM.  Algorithmic bytes: 32 B per
+    trilinear sample (FP), 16 B per bilinear update (BP), SURVEY 8(d)."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    sms = 148
+    mhz = (clocks or {}).get("sm_mhz")
+    if not mhz and p.exists():
+        mhz = json.loads(p.read_text()).get("sm_max_mhz")
+    mhz = float(mhz or 1965.0)
+    peak = 128.0 * sms * mhz * 1e6 / 1e9  # GB/s
+    fp = fp_bytes / (fp_ms * 1e-3) / 1e9
+    bp = bp_bytes / (bp_ms * 1e-3) / 1e9
+    return {"bound": "l1_load_path", "unit": "GB/s", "peak": round(peak, 1),
+            "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)",
+            "forward": {"kernel": FP_KERNEL, "achieved": round(fp, 1), "frac": round(fp / peak, 4),
+                        "bytes_per_unit": "32 B per trilinear sample"},
+            "back": {"kernel": BP_KERNEL, "achieved": round(bp, 1), "frac": round(bp / peak, 4),
+                     "bytes_per_unit": "16 B per voxel-view update"}}
 
 
 def count_samples(geom, step, torch):
@@ -376,6 +399,7 @@ def run_ours(args):
                      "note": "achieved = algorithmic gather bytes (32 B per trilinear sample x exact sample "
                              "count) / CUDA-event kernel time; gathers are served mostly by L1/L2, so "
                              "frac > 1 is possible -- traffic is the DRAM bytes ncu measured"},
+        "gather_roofline": gather_roofline(fp_bytes, fp_ms, 16.0 * bp_updates, bp_ms, clocks),
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,

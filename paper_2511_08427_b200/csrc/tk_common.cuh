@@ -59,4 +59,21 @@ int sm_count();
 // ---- device helpers ---------------------------------------------------------
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
 
+// floor() without the conversion pipe (FRND / F2I are quarter rate): for
+// |x| < 2^22, x + 1.5 * 2^23 rounded toward -inf is exactly 1.5 * 2^23 + floor(x),
+// so the sum's bit pattern is kFloorBits + floor(x) (an integer, usable in
+// index arithmetic modulo 2^32) and sum - kFloorMagic is floor(x) as a float.
+constexpr float kFloorMagic = 12582912.f;
+constexpr unsigned kFloorBits = 0x4B400000u;
+__device__ __forceinline__ float floor_magic(float x) { return __fadd_rd(x, kFloorMagic); }
+
+// base + idx elements as ONE IMAD.WIDE.U32 (keeps the compiler from re-forming
+// 64-bit (outer * stride + idx) << log2(size) chains per gather).
+template <class T>
+__device__ __forceinline__ const T *elem_ptr(const T *base, unsigned idx) {
+  const T *r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "n"((int)sizeof(T)), "l"(base));
+  return r;
+}
+
 }  // namespace tk

@@ -367,19 +367,25 @@ __global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny
   }
 }
 
-template <int MINB>
+// WR = detector rows per warp: lane l takes row l % WR, column l / WR, so a
+// quarter-warp (8 lanes) spans min(WR, 8) rows of one to eight columns.  Rays of
+// one column march through the same (a, b) cells in near lock-step (they
+// differ only in z), so with WR > 1 the cell changes of a quarter coincide.
+template <int MINB, bool MAGIC, int WR = 1>
 __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     cone_fp4_kernel(const float4 *__restrict__ qA, const float4 *__restrict__ qB, int nx, int ny,
                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
                     int rows, int cols, int n_views, double step, float *__restrict__ out) {
-  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  constexpr int kCols = kFp2BX * kFp2BY / WR;  // columns per CTA (CTA = kCols x WR rays)
+  const int ncb = (cols + kCols - 1) / kCols;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
   const unsigned bt = b / ncb;
   const int v = (int)(bt % n_views);
   const int rb = (int)(bt / n_views);
-  const int c = cb * kFp2BX + threadIdx.x;
-  const int r = rb * kFp2BY + threadIdx.y;
+  const int lane = threadIdx.x, warp = threadIdx.y;  // blockDim = (32, 4)
+  const int c = WR == 1 ? cb * kFp2BX + lane : cb * kCols + warp * (32 / WR) + lane / WR;
+  const int r = WR == 1 ? rb * kFp2BY + warp : rb * WR + lane % WR;
   if (c >= cols || r >= rows) return;
   float *dst = out + ((long long)v * rows + r) * cols + c;
   const Fp2View W = views[v];
@@ -401,14 +407,28 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
   float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
   // one trilinear sample at march parameter kk (in steps); the in-slice part
   // of the cell index, lb * pa + la < 2^24, is formed exactly in float
+  const unsigned bias = kFloorBits * (1u + (unsigned)pa + (unsigned)ps);
   auto sample = [&](float kk) -> float {
     const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
-    const float la = floorf(fa), lb = floorf(fb), lz = floorf(fz);
-    const int id = __float2int_rz(lz) * ps + __float2int_rz(fmaf(lb, paf, la));
+    float la, lb, lz;
+    int id;
+    if (MAGIC) {  // floor via FADD.RM (no conversion-pipe instructions), index from the float bits
+      const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
+      id = (int)(__float_as_uint(xz) * (unsigned)ps + (__float_as_uint(xb) * (unsigned)pa + __float_as_uint(xa)));
+      la = xa - kFloorMagic;
+      lb = xb - kFloorMagic;
+      lz = xz - kFloorMagic;
+    } else {
+      la = floorf(fa);
+      lb = floorf(fb);
+      lz = floorf(fz);
+      id = __float2int_rz(lz) * ps + __float2int_rz(fmaf(lb, paf, la));
+    }
     if (id != cell) {
       cell = id;
-      lo4 = __ldg(q + id);
-      hi4 = __ldg(q + id + ps);
+      const float4 *p = MAGIC ? elem_ptr(q, (unsigned)id - bias) : q + id;
+      lo4 = __ldg(p);
+      hi4 = __ldg(p + ps);
     }
     const float wa = fa - la, wb = fb - lb;
     const float s0 = lerpf(lerpf(lo4.x, lo4.y, wa), lerpf(lo4.z, lo4.w, wa), wb);
@@ -490,9 +510,6 @@ __device__ __forceinline__ void ldg_cell8(const Cell8 *p, float (&c)[8]) {
                : "l"(p));
 }
 
-constexpr float kFloorMagic = 12582912.f;  // 1.5 * 2^23: x + M rounded down = M + floor(x)
-constexpr unsigned kFloorBits = 0x4B400000u;
-
 template <int MINB>
 __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     cone_fp8_kernel(const Cell8 *__restrict__ qA, const Cell8 *__restrict__ qB, int nx, int ny,
@@ -528,12 +545,11 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
   float k8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   auto sample = [&](float kk) -> float {
     const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
-    const float xa = __fadd_rd(fa, kFloorMagic), xb = __fadd_rd(fb, kFloorMagic),
-                xz = __fadd_rd(fz, kFloorMagic);
+    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
     const unsigned id = __float_as_uint(xz) * ps + (__float_as_uint(xb) * pa + __float_as_uint(xa));
     if (id != cell) {
       cell = id;
-      ldg_cell8(q + (id - bias), k8);
+      ldg_cell8(elem_ptr(q, id - bias), k8);
     }
     const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
     const float lo = fmaf(wb, fmaf(wa, k8[3], k8[2]), fmaf(wa, k8[1], k8[0]));
@@ -1059,6 +1075,146 @@ __global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_quad_kernel(const BpP
 }
 
 // ---------------------------------------------------------------------------
+// Coefficient-quad back projector ("coef", default).
+//
+// Same traversal as cone_bp_quad_kernel, but
+//   * each quad holds the bilinear polynomial of its detector cell,
+//       C[v][r0+2][c0+2] = (s00, s01 - s00, s10 - s00, s11 - s10 - s01 + s00),
+//     so an update is  acc += q * ((s00 + wc c1) + wr (c2 + wc c3)): 4 FFMA;
+//   * row / column floors use floor_magic (no FRND / F2I), the row index comes
+//     straight from the float bits; rows are clamped in float onto the all-zero
+//     quad rows -2 / R (their weights are irrelevant there).
+// ---------------------------------------------------------------------------
+__global__ void coefify_kernel(const float *__restrict__ sino, int n_views, int rows, int cols,
+                               float4 *__restrict__ quads) {
+  const int qc = cols + 1 + kQuadPad, qr = rows + 1 + kQuadPad;
+  const long long total = (long long)n_views * qr * qc;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % qc) - kQuadPad;
+    const long long t = i / qc;
+    const int r0 = (int)(t % qr) - kQuadPad;
+    const int v = (int)(t / qr);
+    const float *s = sino + (long long)v * rows * cols;
+    const bool ca = (unsigned)c0 < (unsigned)cols, cb = (unsigned)(c0 + 1) < (unsigned)cols;
+    const bool ra = (unsigned)r0 < (unsigned)rows, rb = (unsigned)(r0 + 1) < (unsigned)rows;
+    const float s00 = (ra && ca) ? __ldg(s + (long long)r0 * cols + c0) : 0.f;
+    const float s01 = (ra && cb) ? __ldg(s + (long long)r0 * cols + c0 + 1) : 0.f;
+    const float s10 = (rb && ca) ? __ldg(s + (long long)(r0 + 1) * cols + c0) : 0.f;
+    const float s11 = (rb && cb) ? __ldg(s + (long long)(r0 + 1) * cols + c0 + 1) : 0.f;
+    quads[i] = make_float4(s00, s01 - s00, s10 - s00, (s11 - s10) - (s01 - s00));
+  }
+}
+
+template <int ZB, bool ZINV, bool WEIGHTED>
+__global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_coef_kernel(const BpParams p,
+                                                                   const float4 *__restrict__ quads) {
+  __shared__ ConeVoxView sv[kBpChunk];
+  const int ix = blockIdx.x * kBqBX + threadIdx.x;
+  const int iy = blockIdx.y * kBqBY + threadIdx.y;
+  const int zl0 = blockIdx.z * ZB;
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx;
+  const float yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  const int tid = threadIdx.y * kBqBX + threadIdx.x;
+  const unsigned qc = (unsigned)(p.cols + 1 + kQuadPad);  // quads per row
+  const float rhi = (float)p.band_rows;                   // all-zero quad rows: -2 and R
+  const float chi = (float)p.cols;                        // all-zero quad columns: -2 and C
+  const long long qview = (long long)(p.band_rows + 1 + kQuadPad) * qc;
+  const float colmax = (float)(p.cols - 1);
+  // quad offset of (row r0, column c0) from raw floor bits: (r0 + 2) qc + c0 + 2
+  const unsigned rbias = ((unsigned)kQuadPad - kFloorBits) * qc;
+  const unsigned cbias = (unsigned)kQuadPad - kFloorBits;
+
+  float acc[ZB];
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) acc[k] = 0.f;
+
+  for (int v0 = 0; v0 < p.n_views; v0 += kBpChunk) {
+    const int nch = min(kBpChunk, p.n_views - v0);
+    __syncthreads();
+    for (int i = tid; i < nch * 12; i += kBqBX * kBqBY)
+      reinterpret_cast<float *>(sv)[i] = __ldg(reinterpret_cast<const float *>(p.views + v0) + i);
+    __syncthreads();
+    if (!active) continue;
+    for (int j = 0; j < nch; ++j) {
+      const ConeVoxView &V = sv[j];
+      const float4 *qv = quads + (long long)(v0 + j) * qview;
+      const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+      const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+      const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+      if (ZINV) {
+        if (!(w0 > (float)kTiny)) continue;  // _kernels.py:297-298
+        const float rw = 1.f / w0;
+        const float fc = fmaf(a0, rw, p.cu);
+        const float xcf = floor_magic(fc);
+        const float flc = xcf - kFloorMagic;
+        if (!(flc >= -1.f && flc <= colmax)) continue;  // both column taps off the detector
+        const float wc = fc - flc;
+        float q = 1.f;
+        if (WEIGHTED) {  // (sid / w)^2, _kernels.py:318-320
+          q = p.sid * rw;
+          q *= q;
+        }
+        const unsigned rcb = rbias + __float_as_uint(xcf) + cbias;  // + column, per (x, y, view)
+        const float fr0 = fmaf(b0, rw, p.cv);
+        const float dr = V.b[2] * rw;
+#pragma unroll
+        for (int k0 = 0; k0 < ZB; k0 += 8) {
+          unsigned off[8];
+          float wr[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float fr = fminf(fmaxf(fmaf((float)(k0 + i), dr, fr0), -2.f), rhi);
+            const float xr = floor_magic(fr);
+            off[i] = __float_as_uint(xr) * qc + rcb;
+            wr[i] = fr - (xr - kFloorMagic);
+          }
+          float4 t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = __ldg(elem_ptr(qv, off[i]));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float val = fmaf(wr[i], fmaf(wc, t[i].w, t[i].z), fmaf(wc, t[i].y, t[i].x));
+            acc[k0 + i] = fmaf(q, val, acc[k0 + i]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < ZB; ++k) {
+          const float kf = (float)k;
+          const float w = fmaf(kf, V.w[2], w0);
+          if (!(w > (float)kTiny)) continue;
+          const float rw = 1.f / w;
+          const float fc = fminf(fmaxf(fmaf(fmaf(kf, V.a[2], a0), rw, p.cu), -2.f), chi);
+          const float fr = fminf(fmaxf(fmaf(fmaf(kf, V.b[2], b0), rw, p.cv), -2.f), rhi);
+          const float xcf = floor_magic(fc), xr = floor_magic(fr);
+          const float4 t = __ldg(elem_ptr(qv, __float_as_uint(xr) * qc + rbias + __float_as_uint(xcf) + cbias));
+          const float wc = fc - (xcf - kFloorMagic), wr = fr - (xr - kFloorMagic);
+          const float val = fmaf(wr, fmaf(wc, t.w, t.z), fmaf(wc, t.y, t.x));
+          if (WEIGHTED) {
+            const float q = p.sid * rw;
+            acc[k] = fmaf(q * q, val, acc[k]);
+          } else {
+            acc[k] += val;
+          }
+        }
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < ZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Shared-memory staged back projector ("smem", default for z-invariant
 // trajectories) -- the north star's "detector tiles for a batch of views are
 // staged into shared memory".
@@ -1428,8 +1584,8 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg8 (default) | ldg4 | ldg2 | ldg | tex | hwtex.
-enum class FpAlgo { kLdg8, kLdg4, kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg4m (default) | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
@@ -1438,7 +1594,8 @@ static FpAlgo fp_algo() {
   if (e && !strcmp(e, "ldg2")) return FpAlgo::kLdg2;
   if (e && !strcmp(e, "tex")) return FpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
-  return FpAlgo::kLdg8;
+  if (e && !strcmp(e, "ldg8")) return FpAlgo::kLdg8;
+  return FpAlgo::kLdg4m;
 }
 
 // A forward-projection plan: the two orientation copies of one volume (8-
@@ -1460,7 +1617,7 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->sz = sz;
   plan->sy = sy;
   plan->sx = sx;
-  plan->coef = fp_algo() != FpAlgo::kLdg4;
+  plan->coef = fp_algo() == FpAlgo::kLdg8;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
@@ -1500,7 +1657,11 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
   dim3 block(kFp2BX, kFp2BY);
-  const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
+  const char *wre = getenv("TK_FP_WR");  // detector rows per warp (1, 4 or 8; ldg4 / ldg4m only)
+  const int wr = (!pl.coef && wre) ? atoi(wre) : 1;
+  const bool wide = wr == 4 || wr == 8;
+  const int bc = wide ? kFp2BX * kFp2BY / wr : kFp2BX, br = wide ? wr : kFp2BY;
+  const long long nblocks = (long long)ceil_div(cols, bc) * ceil_div(rows, br) * n_views;
   if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
   const char *mb = getenv("TK_FP2_MINB");  // 8, 10 or 12 resident CTAs per SM
   const int minb = mb ? atoi(mb) : 12;  // 12 CTAs x 128 threads (<= 40 regs): measured best for ldg4
@@ -1511,7 +1672,11 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
   } else {
-    auto kern = minb >= 12 ? cone_fp4_kernel<12> : cone_fp4_kernel<10>;
+    const bool magic = fp_algo() == FpAlgo::kLdg4m;
+    auto kern = minb >= 12 ? (magic ? cone_fp4_kernel<12, true> : cone_fp4_kernel<12, false>)
+                           : (magic ? cone_fp4_kernel<10, true> : cone_fp4_kernel<10, false>);
+    if (magic && wr == 4) kern = cone_fp4_kernel<12, true, 4>;
+    if (magic && wr == 8) kern = cone_fp4_kernel<12, true, 8>;
     kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const float4 *>(pl.qA), static_cast<const float4 *>(pl.qB),
                                               pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
                                               cols, n_views, step, out);
@@ -1591,7 +1756,7 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
-  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4))
+  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m))
     return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
@@ -1634,11 +1799,12 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   return TK_OK;
 }
 
-// Back-projector algorithm: TK_BP_ALGO = ldg (default) | tex | hwtex.
-enum class BpAlgo { kSmem, kQuad, kLdg, kTex, kHwTex };
+// Back-projector algorithm: TK_BP_ALGO = quad (default) | coef | smem | ldg | tex | hwtex.
+enum class BpAlgo { kCoef, kSmem, kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
+  if (e && !strcmp(e, "coef")) return BpAlgo::kCoef;
   if (e && !strcmp(e, "smem")) return BpAlgo::kSmem;
   if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
@@ -1665,26 +1831,36 @@ static int launch_bp_smem(const BpParams &p, bool weighted, cudaStream_t st) {
   return TK_OK;
 }
 
-static int launch_bp_quad(BpParams p, bool weighted, bool zinv, cudaStream_t st) {
+static int launch_bp_quad(BpParams p, bool weighted, bool zinv, bool coef, cudaStream_t st) {
   const long long qview = (long long)(p.band_rows + 1 + kQuadPad) * (p.cols + 1 + kQuadPad);
   const long long nq = qview * p.n_views;
   Scratch quads;
   TK_TRY_CUDA(quads.alloc(sizeof(float4) * nq, st));
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(nq, 256), (long long)sm_count() * 32);
-  quadify_kernel<<<qgrid, 256, 0, st>>>(p.sino, p.n_views, p.band_rows, p.cols, quads.as<float4>());
-  TK_LAUNCHED("quadify_kernel");
+  if (coef) {
+    coefify_kernel<<<qgrid, 256, 0, st>>>(p.sino, p.n_views, p.band_rows, p.cols, quads.as<float4>());
+    TK_LAUNCHED("coefify_kernel");
+  } else {
+    quadify_kernel<<<qgrid, 256, 0, st>>>(p.sino, p.n_views, p.band_rows, p.cols, quads.as<float4>());
+    TK_LAUNCHED("quadify_kernel");
+  }
   dim3 block(kBqBX, kBqBY);
   dim3 grid(ceil_div(p.nx, kBqBX), ceil_div(p.ny, kBqBY), ceil_div(p.z_count, kBqZB));
   const float4 *q = quads.as<float4>();
-  if (zinv && weighted)
-    cone_bp_quad_kernel<kBqZB, true, true><<<grid, block, 0, st>>>(p, q);
-  else if (zinv)
-    cone_bp_quad_kernel<kBqZB, true, false><<<grid, block, 0, st>>>(p, q);
-  else if (weighted)
-    cone_bp_quad_kernel<kBqZB, false, true><<<grid, block, 0, st>>>(p, q);
-  else
-    cone_bp_quad_kernel<kBqZB, false, false><<<grid, block, 0, st>>>(p, q);
-  TK_LAUNCHED("cone_bp_quad_kernel");
+  const int sel = (zinv ? 2 : 0) + (weighted ? 1 : 0);
+  if (coef) {
+    if (sel == 3) cone_bp_coef_kernel<kBqZB, true, true><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 2) cone_bp_coef_kernel<kBqZB, true, false><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 1) cone_bp_coef_kernel<kBqZB, false, true><<<grid, block, 0, st>>>(p, q);
+    else cone_bp_coef_kernel<kBqZB, false, false><<<grid, block, 0, st>>>(p, q);
+    TK_LAUNCHED("cone_bp_coef_kernel");
+  } else {
+    if (sel == 3) cone_bp_quad_kernel<kBqZB, true, true><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 2) cone_bp_quad_kernel<kBqZB, true, false><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 1) cone_bp_quad_kernel<kBqZB, false, true><<<grid, block, 0, st>>>(p, q);
+    else cone_bp_quad_kernel<kBqZB, false, false><<<grid, block, 0, st>>>(p, q);
+    TK_LAUNCHED("cone_bp_quad_kernel");
+  }
   return TK_OK;
 }
 
@@ -1823,7 +1999,8 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   p.tex = 0;
   BpAlgo algo = bp_algo();
   if (algo == BpAlgo::kSmem && zinv) return launch_bp_smem(p, weighted != 0, st);
-  if (algo == BpAlgo::kQuad || algo == BpAlgo::kSmem) return launch_bp_quad(p, weighted != 0, zinv, st);
+  if (algo == BpAlgo::kCoef || algo == BpAlgo::kQuad || algo == BpAlgo::kSmem)
+    return launch_bp_quad(p, weighted != 0, zinv, algo == BpAlgo::kCoef, st);
   if (n_views > 2048) algo = BpAlgo::kLdg;  // layered arrays hold <= 2048 layers
   TexLease lease;
   if (algo != BpAlgo::kLdg) {

@@ -315,6 +315,314 @@ __global__ void __launch_bounds__(32 * kFwWarps) fft_filter_warp_kernel(const Fi
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident radix-16 variant ("r16", default for 512 <= n_pad <= 8192).
+//
+// T = n_pad / 16 threads own one row pair; every thread holds 16 complex
+// values.  Forward plan [16, 16, ..., r_last] (Stockham), inverse plan the
+// mirror image [r_last, ..., 16]: the forward's last stage leaves thread t with
+// the spectrum bins  j + (N / r_last) * r  of its butterflies j -- exactly the
+// inputs of the inverse's first (Ns = 1) stage, so the frequency weights, the
+// conjugation and that first inverse butterfly run on registers with no
+// shared-memory round trip.  Shared memory (ping-pong, one barrier per
+// exchange) only carries the data between the other stages.  The obliquity
+// pre-weight's row term is computed once per row, not per sample.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dft16(float2 *v) {
+  float2 e[8], o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  dft8(e);
+  dft8(o);
+  // o[k] *= W16^k = exp(-2 pi i k / 16)
+  const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
+  const float r2 = 0.70710678118654752440f;
+  const float2 w[8] = {{1.f, 0.f}, {c1, -s1}, {r2, -r2}, {s1, -c1},
+                       {0.f, -1.f}, {-s1, -c1}, {-r2, -r2}, {-c1, -s1}};
+#pragma unroll
+  for (int k = 1; k < 8; ++k) o[k] = cmul(o[k], w[k]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    v[k] = cadd(e[k], o[k]);
+    v[k + 8] = csub(e[k], o[k]);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void dft_r(float2 *v) {
+  if constexpr (R == 16) dft16(v);
+  if constexpr (R == 8) dft8(v);
+  if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
+  if constexpr (R == 2) dft2(v);
+}
+
+template <int LOGN>
+struct R16Plan {
+  static constexpr int kN = 1 << LOGN;
+  static constexpr int kT = kN / 16;                    // threads per row pair
+  static constexpr int kFull = LOGN / 4;                // radix-16 stages
+  static constexpr int kRem = LOGN % 4;                 // last radix 2^kRem (0: none)
+  static constexpr int kStages = kFull + (kRem ? 1 : 0);
+  static constexpr int radix(int s) { return s < kFull ? 16 : (1 << kRem); }     // forward
+  static constexpr int iradix(int s) { return radix(kStages - 1 - s); }          // inverse
+  static constexpr int span(int s) { return s == 0 ? 1 : span(s - 1) * radix(s - 1); }
+  static constexpr int ispan(int s) { return s == 0 ? 1 : ispan(s - 1) * iradix(s - 1); }
+  // per-stage twiddle tables (w1[NS], w4[NS]) for stages 1..kStages-1, forward then inverse
+  static constexpr int fwd_off(int s) { return s <= 1 ? 0 : fwd_off(s - 1) + 2 * span(s - 1); }
+  static constexpr int inv_off(int s) {
+    return s <= 1 ? fwd_off(kStages) : inv_off(s - 1) + 2 * ispan(s - 1);
+  }
+  static constexpr int kTabs = inv_off(kStages);
+};
+
+__device__ __forceinline__ int r16_pad(int e) { return e + (e >> 4); }
+
+// Twiddles W_{Ns R}^{r k}, r = 1..R-1, from two table entries w1 = W^k and
+// w4 = W^{4k} (per-stage tables indexed by k: conflict-free shared loads; the
+// full-circle table indexed by r k stride is 8- to 16-way bank conflicted).
+// Products are at most four deep (a few ulp, far inside the 1e-4 budget).
+template <int R>
+__device__ __forceinline__ void apply_twiddles(float2 *v, float2 w1, float2 w4) {
+  if constexpr (R == 2) {
+    v[1] = cmul(v[1], w1);
+  } else {
+    const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    if constexpr (R >= 8) {
+      v[4] = cmul(v[4], w4);
+      v[5] = cmul(v[5], cmul(w4, w1));
+      v[6] = cmul(v[6], cmul(w4, w2));
+      v[7] = cmul(v[7], cmul(w4, w3));
+    }
+    if constexpr (R == 16) {
+      const float2 w8 = cmul(w4, w4), w12 = cmul(w8, w4);
+      v[8] = cmul(v[8], w8);
+      v[9] = cmul(v[9], cmul(w8, w1));
+      v[10] = cmul(v[10], cmul(w8, w2));
+      v[11] = cmul(v[11], cmul(w8, w3));
+      v[12] = cmul(v[12], w12);
+      v[13] = cmul(v[13], cmul(w12, w1));
+      v[14] = cmul(v[14], cmul(w12, w2));
+      v[15] = cmul(v[15], cmul(w12, w3));
+    }
+  }
+}
+
+// One Stockham stage on registers v[16] (16/R butterflies per thread):
+// twiddles (stage table `tab`: NS entries w1 then NS entries w4), then the DFT.
+template <int R, int N, int NS>
+__device__ __forceinline__ void r16_butterflies(float2 *v, const float2 *__restrict__ tab) {
+  constexpr int kB = 16 / R;
+#pragma unroll
+  for (int c = 0; c < kB; ++c) {
+    const int j = threadIdx.x * kB + c;
+    const int k = j & (NS - 1);
+    if constexpr (NS > 1) apply_twiddles<R>(v + c * R, tab[k], tab[NS + k]);
+    dft_r<R>(v + c * R);
+  }
+}
+
+template <int R, int N, int NS>
+__device__ __forceinline__ void r16_gather(float2 *v, const float2 *__restrict__ buf) {
+  constexpr int kB = 16 / R;
+  constexpr int nb = N / R;
+#pragma unroll
+  for (int c = 0; c < kB; ++c) {
+    const int j = threadIdx.x * kB + c;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[c * R + r] = buf[r16_pad(j + r * nb)];
+  }
+}
+
+template <int R, int N, int NS>
+__device__ __forceinline__ void r16_scatter(const float2 *v, float2 *__restrict__ buf) {
+  constexpr int kB = 16 / R;
+#pragma unroll
+  for (int c = 0; c < kB; ++c) {
+    const int j = threadIdx.x * kB + c;
+    const int k = j & (NS - 1);
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[r16_pad(base + r * NS)] = v[c * R + r];
+  }
+}
+
+template <int LOGN, int S>
+__device__ __forceinline__ void r16_forward(float2 *v, float2 *b0, float2 *b1, const float2 *tw) {
+  using P = R16Plan<LOGN>;
+  if constexpr (S < P::kStages) {
+    constexpr int R = P::radix(S), NS = P::span(S);
+    if constexpr (S > 0) {  // stage S reads buffer (S-1)&1
+      r16_gather<R, P::kN, NS>(v, ((S - 1) & 1) ? b1 : b0);
+    }
+    r16_butterflies<R, P::kN, NS>(v, tw + P::fwd_off(S));
+    if constexpr (S < P::kStages - 1) {
+      r16_scatter<R, P::kN, NS>(v, (S & 1) ? b1 : b0);
+      __syncthreads();
+    }
+    r16_forward<LOGN, S + 1>(v, b0, b1, tw);
+  }
+}
+
+// inverse stages 1.. (stage 0 runs on registers in the kernel body and
+// scatters to buffer X0); stage S reads buffer X0 ^ ((S-1)&1), writes X0 ^ (S&1)
+template <int LOGN, int X0, int S>
+__device__ __forceinline__ void r16_inverse(float2 *v, float2 *b0, float2 *b1, const float2 *tw) {
+  using P = R16Plan<LOGN>;
+  if constexpr (S < P::kStages) {
+    constexpr int R = P::iradix(S), NS = P::ispan(S);
+    r16_gather<R, P::kN, NS>(v, (X0 ^ ((S - 1) & 1)) ? b1 : b0);
+    r16_butterflies<R, P::kN, NS>(v, tw + P::inv_off(S));
+    if constexpr (S < P::kStages - 1) {
+      r16_scatter<R, P::kN, NS>(v, (X0 ^ (S & 1)) ? b1 : b0);
+      __syncthreads();
+    }
+    r16_inverse<LOGN, X0, S + 1>(v, b0, b1, tw);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(R16Plan<LOGN>::kT, 512 / R16Plan<LOGN>::kT) fft_filter_r16_kernel(const FilterParams p) {
+  using P = R16Plan<LOGN>;
+  constexpr int N = P::kN, T = P::kT;
+  constexpr int padN = N + N / 16;
+  constexpr int kX0 = 1 - ((P::kStages - 2) & 1);  // buffer not read by the last forward stage
+  extern __shared__ float smem[];
+  float2 *b0 = reinterpret_cast<float2 *>(smem);
+  float2 *b1 = b0 + padN;
+  float2 *tw = b1 + padN;  // per-stage twiddle tables (R16Plan::kTabs entries)
+  float *wgt = reinterpret_cast<float *>(tw + P::kTabs);
+  for (int i = threadIdx.x; i < P::kTabs; i += T) {
+    // locate stage (forward s or inverse s) and entry of table slot i
+    int ns = 1, r = 1, base = 0;
+    bool found = false;
+#pragma unroll
+    for (int st = 1; st < P::kStages; ++st) {
+      if (!found && i >= P::fwd_off(st) && i < P::fwd_off(st) + 2 * P::span(st)) {
+        ns = P::span(st), r = P::radix(st), base = P::fwd_off(st), found = true;
+      }
+      if (!found && i >= P::inv_off(st) && i < P::inv_off(st) + 2 * P::ispan(st)) {
+        ns = P::ispan(st), r = P::iradix(st), base = P::inv_off(st), found = true;
+      }
+    }
+    const int e = i - base, k = e % ns, mult = e < ns ? 1 : 4;
+    const int tstride = N / (ns * r);  // W_{ns r}^{mult k} = W_N^{mult k tstride}
+    tw[i] = p.tw[(mult * k * tstride) & (N - 1)];
+  }
+  for (int i = threadIdx.x; i <= N / 2; i += T) wgt[i] = p.wgt[i];
+  __syncthreads();
+  const bool pre = p.sdd > 0.f;
+  const float ucen = 0.5f * (float)(p.width - 1), vcen = 0.5f * (float)(p.det_rows - 1);
+  const float sdd2 = p.sdd * p.sdd;
+  const long long n_pairs = (p.n_rows + 1) / 2;
+  for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
+    const long long ra = 2 * pair, rb = ra + 1;
+    const bool has_b = rb < p.n_rows;
+    const float *ia = p.in + ra * p.width;
+    const float *ib = p.in + rb * p.width;
+    // obliquity pre-weight: row term once per row (reference filters.py:154-171)
+    float qa = 0.f, qb = 0.f;
+    if (pre) {
+      const float va = ((float)((int)(ra % p.band_rows) + p.row_offset) - vcen) * p.dv;
+      const float vb = ((float)((int)(rb % p.band_rows) + p.row_offset) - vcen) * p.dv;
+      qa = fmaf(va, va, sdd2);
+      qb = fmaf(vb, vb, sdd2);
+    }
+    float2 v[16];
+    {  // forward stage 0 (Ns = 1) reads the zero-padded rows straight from global
+      constexpr int R0 = P::radix(0), kB = 16 / R0, nb = N / R0;
+#pragma unroll
+      for (int c = 0; c < kB; ++c) {
+        const int j = threadIdx.x * kB + c;
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+          const int e = j + r * nb;
+          float a = 0.f, b = 0.f;
+          if (e < p.width) {
+            a = __ldg(ia + e);
+            if (has_b) b = __ldg(ib + e);
+            if (pre) {
+              const float u = ((float)e - ucen) * p.du;
+              a *= p.sdd * rsqrtf(fmaf(u, u, qa));
+              b *= p.sdd * rsqrtf(fmaf(u, u, qb));
+            }
+          }
+          v[c * R0 + r] = make_float2(a, b);
+        }
+      }
+    }
+    r16_forward<LOGN, 0>(v, b0, b1, tw);
+    {  // weights (real, even, scale / N folded in), conjugate, inverse stage 0 -- on registers
+      constexpr int RL = P::radix(P::kStages - 1), kB = 16 / RL, nb = N / RL;
+#pragma unroll
+      for (int c = 0; c < kB; ++c) {
+        const int j = threadIdx.x * kB + c;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int e = j + r * nb;
+          const float w = wgt[e <= N / 2 ? e : N - e];
+          v[c * RL + r] = make_float2(v[c * RL + r].x * w, -v[c * RL + r].y * w);
+        }
+        dft_r<RL>(v + c * RL);
+      }
+      if constexpr (P::kStages > 1) {
+        // the forward's last stage may still be reading buffer ((F-1)&1): write the other
+        r16_scatter<RL, N, 1>(v, kX0 ? b1 : b0);
+        __syncthreads();
+      }
+    }
+    r16_inverse<LOGN, kX0, 1>(v, b0, b1, tw);
+    {  // last inverse stage: outputs j + (N / R) r in natural order -> conj, crop, store
+      constexpr int S = P::kStages - 1;
+      constexpr int R = P::iradix(S), NS = P::ispan(S), kB = 16 / R;
+      float *oa = p.out + ra * p.width;
+      float *ob = p.out + rb * p.width;
+#pragma unroll
+      for (int c = 0; c < kB; ++c) {
+        const int j = threadIdx.x * kB + c;
+        const int k = j & (NS - 1);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int o = base + r * NS;
+          if (o < p.width) {
+            oa[o] = v[c * R + r].x;
+            if (has_b) ob[o] = -v[c * R + r].y;
+          }
+        }
+      }
+    }
+    __syncthreads();  // buffers are reused by the next pair
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_filter_r16(const FilterParams &p, cudaStream_t st) {
+  using P = R16Plan<LOGN>;
+  constexpr int N = P::kN;
+  const size_t smem = sizeof(float2) * (2 * (N + N / 16) + P::kTabs) + sizeof(float) * (N / 2 + 1);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fft_filter_r16_kernel<LOGN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fft_filter_r16_kernel<LOGN>,
+                                                                P::kT, smem);
+  if (e != cudaSuccess) return e;
+  const long long pairs = (p.n_rows + 1) / 2;
+  const unsigned grid = (unsigned)std::min<long long>(pairs, (long long)sm_count() * std::max(1, per_sm));
+  fft_filter_r16_kernel<LOGN><<<grid, P::kT, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 static cudaError_t launch_filter_warp(const FilterParams &p, cudaStream_t st) {
   constexpr int N = 1 << LOGN;
@@ -335,9 +643,12 @@ static cudaError_t launch_filter_warp(const FilterParams &p, cudaStream_t st) {
 template <int LOGN>
 static cudaError_t launch_filter(const FilterParams &p, size_t smem, cudaStream_t st) {
   constexpr int N = 1 << LOGN;
+  const char *algo = getenv("TK_FILTER_ALGO");  // r16 (default) | stockham | warp
+  if constexpr (LOGN >= 9 && LOGN <= 13) {
+    if (!algo || !strcmp(algo, "r16")) return launch_filter_r16<LOGN>(p, st);
+  }
   if (LOGN <= 11) {  // TK_FILTER_ALGO=warp: warp-per-row-pair variant (measured slower at cfg4)
-    const char *e = getenv("TK_FILTER_ALGO");
-    if (e && !strcmp(e, "warp")) return launch_filter_warp<LOGN>(p, st);
+    if (algo && !strcmp(algo, "warp")) return launch_filter_warp<LOGN>(p, st);
   }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fft_filter_kernel<LOGN>,

@@ -32,14 +32,19 @@ geom = full if a.views == 720 else tk.GeometryCone3D(full.volume_shape, full.vol
 vol = tk.phantoms.shepp_logan_3d(geom.volume_shape)
 sino = torch.empty(geom.sinogram_shape, device="cuda")
 fp_tensor(vol, geom, 0.25, out=sino)
-filt = filter_stage_tensor(sino, geom, "shepp_logan") if a.op == "bp" else None
+filt = filter_stage_tensor(sino, geom, "shepp_logan") if a.op in ("bp", "filter") else None
 out = torch.empty(geom.volume_shape, device="cuda")
 ref = None
 res = {}
 for cfg in a.configs.split(";"):
     env = dict(kv.split("=") for kv in cfg.split(",") if kv)
     os.environ.update(env)
-    fn = (lambda: fp_tensor(vol, geom, 0.25, out=sino)) if a.op == "fp" else (lambda: bp_tensor(filt, geom, True, out=out))
+    if a.op == "fp":
+        fn = lambda: fp_tensor(vol, geom, 0.25, out=sino)  # noqa: E731
+    elif a.op == "filter":
+        fn = lambda: filter_stage_tensor(sino, geom, "shepp_logan", out=filt)  # noqa: E731
+    else:
+        fn = lambda: bp_tensor(filt, geom, True, out=out)  # noqa: E731
     fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -50,7 +55,7 @@ for cfg in a.configs.split(";"):
         e.record()
         torch.cuda.synchronize()
         best = min(best, s.elapsed_time(e))
-    res_t = sino if a.op == "fp" else out
+    res_t = {"fp": sino, "filter": filt}.get(a.op, out)
     if ref is None:
         ref = res_t.clone()
     err = float(torch.linalg.vector_norm((res_t - ref).double()) / torch.linalg.vector_norm(ref.double()))

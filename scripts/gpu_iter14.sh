@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out
+python __graft_entry__.py build > gpurun_out/build.log 2>&1; echo build rc=$?
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_i14.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_i14.log
+timeout 600 python scripts/fp_sweep.py --op filter --reps 5 --configs "TK_FILTER_ALGO=stockham;TK_FILTER_ALGO=r16" > gpurun_out/sweep_filt14.log 2>&1; echo sweep rc=$?
+cat gpurun_out/sweep_filt14.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fft_filter_r16" -c 1 -o gpurun_out/prof_filt python scripts/prof_step.py --what fdk > gpurun_out/ncu_filt.log 2>&1; echo ncu rc=$?
+timeout 1200 python bench.py > gpurun_out/bench_i14.json 2> gpurun_out/bench_i14.err; echo bench rc=$?
+cat gpurun_out/bench_i14.json

@@ -377,7 +377,7 @@ class TestProperties:
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("algo", ["ldg4", "ldg2", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["ldg4m", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
 def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     monkeypatch.setenv("TK_FP_ALGO", algo)
     geom = tk.GeometryCone3D((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4),
@@ -395,7 +395,7 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     assert rel(got, want) < TOL
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "coef", "ldg", "tex"])
 def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     monkeypatch.setenv("TK_BP_ALGO", algo)
     geom = cone(tk, 24, 36, 1.5, 19)
@@ -409,7 +409,7 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "coef", "ldg", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
@@ -527,3 +527,23 @@ def test_helical_learned_reconstruction_gradient_step(tk):
             x2 = x - t * g
             loss2 = 0.5 * ((tk.ConeProjection3D.apply(x2, geom) - y) ** 2).sum()
         assert float(loss2) < float(loss)
+
+
+@pytest.mark.parametrize("algo", ["r16", "stockham", "warp"])
+@pytest.mark.parametrize("cols,rows,views", [(7, 3, 2), (200, 5, 3), (256, 9, 2), (300, 4, 3), (513, 3, 2),
+                                             (1024, 6, 3), (2047, 2, 1), (3000, 2, 1)])
+def test_filter_variants_match_oracle(tk, oracle, monkeypatch, algo, cols, rows, views):
+    """Every row-filter kernel (TK_FILTER_ALGO) against numpy's rfft/irfft oracle,
+    n_pad from 16 to 8192, odd pair counts, cone pre-weight and a row band."""
+    monkeypatch.setenv("TK_FILTER_ALGO", algo)
+    geom = tk.circular_cone_geometry((8, 8, 8), (1.0, 1.0, 1.0), (rows, cols), (0.7, 0.55), views,
+                                     2 * np.pi, 1200.0, 750.0)
+    y = np.random.default_rng(cols).standard_normal((views, rows, cols))
+    got = tk.filter_stage(tk.Sinogram(T(y), (0.7, 0.55)), geom, "shepp_logan").data
+    want = oracle.filter_stage_cone(y, 1200.0, 750.0, (0.7, 0.55), "shepp_logan")
+    assert rel(got, want) < TOL
+    from paper_2511_08427_b200.filters import filter_stage_tensor
+
+    if rows > 2:  # band of detector rows [1, rows-1) with the global row offset
+        band = filter_stage_tensor(T(y[:, 1:rows - 1]).contiguous(), geom, "shepp_logan", row_offset=1)
+        assert rel(band, want[:, 1:rows - 1]) < TOL
