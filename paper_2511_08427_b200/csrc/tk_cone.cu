@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     cone_fp4_kernel(const float4 *__restrict__ qA, const float4 *__restrict__ qB, int nx, int ny,
                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
                     int rows, int cols, int n_views, double step, float *__restrict__ out) {
-  constexpr int kCols = kFp2BX * kFp2BY / WR;  // columns per CTA (CTA = kCols x WR rays)
+  constexpr int kCols = WR == 1 ? kFp2BX : kFp2BX * kFp2BY / WR;  // columns per CTA
   const int ncb = (cols + kCols - 1) / kCols;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
@@ -966,12 +966,22 @@ __global__ void quadify_kernel(const float *__restrict__ sino, int n_views, int 
   }
 }
 
-template <int ZB, bool ZINV, bool WEIGHTED>
+// Q42: a quarter-warp (the 8 lanes whose 16-byte loads share one L1 data
+// wavefront per 128-byte line) covers 4 x 2 (x, y) voxels instead of 8 x 1, a
+// tighter detector footprint (fewer lines per quarter).
+template <int ZB, bool ZINV, bool WEIGHTED, bool Q42 = false>
 __global__ void __launch_bounds__(kBqBX *kBqBY, 2) cone_bp_quad_kernel(const BpParams p,
                                                                    const float4 *__restrict__ quads) {
   __shared__ ConeVoxView sv[kBpChunk];
-  const int ix = blockIdx.x * kBqBX + threadIdx.x;
-  const int iy = blockIdx.y * kBqBY + threadIdx.y;
+  int ix, iy;
+  if (Q42) {
+    const int t = threadIdx.y * kBqBX + threadIdx.x, w = t >> 5, l = t & 31;
+    ix = blockIdx.x * kBqBX + (l & 3) + 4 * ((l >> 3) & 1);
+    iy = blockIdx.y * kBqBY + 4 * w + ((l >> 2) & 1) + 2 * (l >> 4);
+  } else {
+    ix = blockIdx.x * kBqBX + threadIdx.x;
+    iy = blockIdx.y * kBqBY + threadIdx.y;
+  }
   const int zl0 = blockIdx.z * ZB;
   const bool active = ix < p.nx && iy < p.ny;
   const float xc = (float)ix - p.cx;
@@ -1854,6 +1864,12 @@ static int launch_bp_quad(BpParams p, bool weighted, bool zinv, bool coef, cudaS
     else if (sel == 1) cone_bp_coef_kernel<kBqZB, false, true><<<grid, block, 0, st>>>(p, q);
     else cone_bp_coef_kernel<kBqZB, false, false><<<grid, block, 0, st>>>(p, q);
     TK_LAUNCHED("cone_bp_coef_kernel");
+  } else if (!getenv("TK_BP_Q42") || atoi(getenv("TK_BP_Q42")) != 0) {  // 4x2 quarter-warps (default)
+    if (sel == 3) cone_bp_quad_kernel<kBqZB, true, true, true><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 2) cone_bp_quad_kernel<kBqZB, true, false, true><<<grid, block, 0, st>>>(p, q);
+    else if (sel == 1) cone_bp_quad_kernel<kBqZB, false, true, true><<<grid, block, 0, st>>>(p, q);
+    else cone_bp_quad_kernel<kBqZB, false, false, true><<<grid, block, 0, st>>>(p, q);
+    TK_LAUNCHED("cone_bp_quad_kernel");
   } else {
     if (sel == 3) cone_bp_quad_kernel<kBqZB, true, true><<<grid, block, 0, st>>>(p, q);
     else if (sel == 2) cone_bp_quad_kernel<kBqZB, true, false><<<grid, block, 0, st>>>(p, q);

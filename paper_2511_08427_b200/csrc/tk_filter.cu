@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(32 * kFwWarps) fft_filter_warp_kernel(const Fi
 }
 
 // ---------------------------------------------------------------------------
-// Register-resident radix-16 variant ("r16", default for 512 <= n_pad <= 8192).
+// Register-resident radix-16 variant ("r16", default for 512 <= n_pad <= 4096).
 //
 // T = n_pad / 16 threads own one row pair; every thread holds 16 complex
 // values.  Forward plan [16, 16, ..., r_last] (Stockham), inverse plan the
@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(R16Plan<LOGN>::kT, 512 / R16Plan<LOGN>::kT) ff
   float2 *b1 = b0 + padN;
   float2 *tw = b1 + padN;  // per-stage twiddle tables (R16Plan::kTabs entries)
   float *wgt = reinterpret_cast<float *>(tw + P::kTabs);
+  float *stage_in = wgt + (N / 2 + 1);  // next row pair (N/2 + N/2 floats), filled by cp.async
   for (int i = threadIdx.x; i < P::kTabs; i += T) {
     // locate stage (forward s or inverse s) and entry of table slot i
     int ns = 1, r = 1, base = 0;
@@ -520,11 +521,38 @@ __global__ void __launch_bounds__(R16Plan<LOGN>::kT, 512 / R16Plan<LOGN>::kT) ff
   const float ucen = 0.5f * (float)(p.width - 1), vcen = 0.5f * (float)(p.det_rows - 1);
   const float sdd2 = p.sdd * p.sdd;
   const long long n_pairs = (p.n_rows + 1) / 2;
+  // Each thread stages exactly the input elements it consumes in forward stage
+  // 0 (e = j + r N/16), so the prefetch of pair k+1 needs no barrier: it is
+  // issued after this thread has read pair k's values into registers, and
+  // lands while the rest of pair k's transforms run.
+  constexpr int R0 = P::radix(0), kB0 = 16 / R0, nb0 = N / R0;
+  auto prefetch = [&](long long pr) {
+    if (pr >= n_pairs) return;
+    const long long r0 = 2 * pr;
+    const bool hb = r0 + 1 < p.n_rows;
+    const float *ga = p.in + r0 * p.width, *gb = ga + p.width;
+#pragma unroll
+    for (int c = 0; c < kB0; ++c) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int e = threadIdx.x * kB0 + c + r * nb0;
+        if (e < p.width) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(stage_in + e);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ga + e));
+          if (hb) {
+            const unsigned sb = (unsigned)__cvta_generic_to_shared(stage_in + N / 2 + e);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb), "l"(gb + e));
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  prefetch(blockIdx.x);
   for (long long pair = blockIdx.x; pair < n_pairs; pair += gridDim.x) {
     const long long ra = 2 * pair, rb = ra + 1;
     const bool has_b = rb < p.n_rows;
-    const float *ia = p.in + ra * p.width;
-    const float *ib = p.in + rb * p.width;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     // obliquity pre-weight: row term once per row (reference filters.py:154-171)
     float qa = 0.f, qb = 0.f;
     if (pre) {
@@ -534,18 +562,17 @@ __global__ void __launch_bounds__(R16Plan<LOGN>::kT, 512 / R16Plan<LOGN>::kT) ff
       qb = fmaf(vb, vb, sdd2);
     }
     float2 v[16];
-    {  // forward stage 0 (Ns = 1) reads the zero-padded rows straight from global
-      constexpr int R0 = P::radix(0), kB = 16 / R0, nb = N / R0;
+    {  // forward stage 0 (Ns = 1): the zero-padded rows from this thread's staged elements
 #pragma unroll
-      for (int c = 0; c < kB; ++c) {
-        const int j = threadIdx.x * kB + c;
+      for (int c = 0; c < kB0; ++c) {
+        const int j = threadIdx.x * kB0 + c;
 #pragma unroll
         for (int r = 0; r < R0; ++r) {
-          const int e = j + r * nb;
+          const int e = j + r * nb0;
           float a = 0.f, b = 0.f;
           if (e < p.width) {
-            a = __ldg(ia + e);
-            if (has_b) b = __ldg(ib + e);
+            a = stage_in[e];
+            if (has_b) b = stage_in[N / 2 + e];
             if (pre) {
               const float u = ((float)e - ucen) * p.du;
               a *= p.sdd * rsqrtf(fmaf(u, u, qa));
@@ -556,6 +583,7 @@ __global__ void __launch_bounds__(R16Plan<LOGN>::kT, 512 / R16Plan<LOGN>::kT) ff
         }
       }
     }
+    prefetch(pair + gridDim.x);
     r16_forward<LOGN, 0>(v, b0, b1, tw);
     {  // weights (real, even, scale / N folded in), conjugate, inverse stage 0 -- on registers
       constexpr int RL = P::radix(P::kStages - 1), kB = 16 / RL, nb = N / RL;
@@ -605,7 +633,7 @@ template <int LOGN>
 static cudaError_t launch_filter_r16(const FilterParams &p, cudaStream_t st) {
   using P = R16Plan<LOGN>;
   constexpr int N = P::kN;
-  const size_t smem = sizeof(float2) * (2 * (N + N / 16) + P::kTabs) + sizeof(float) * (N / 2 + 1);
+  const size_t smem = sizeof(float2) * (2 * (N + N / 16) + P::kTabs) + sizeof(float) * (N / 2 + 1 + N);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(fft_filter_r16_kernel<LOGN>,
@@ -644,7 +672,7 @@ template <int LOGN>
 static cudaError_t launch_filter(const FilterParams &p, size_t smem, cudaStream_t st) {
   constexpr int N = 1 << LOGN;
   const char *algo = getenv("TK_FILTER_ALGO");  // r16 (default) | stockham | warp
-  if constexpr (LOGN >= 9 && LOGN <= 13) {
+  if constexpr (LOGN >= 9 && LOGN <= 12) {  // n_pad 8192 needs > 227 KB of tables + buffers
     if (!algo || !strcmp(algo, "r16")) return launch_filter_r16<LOGN>(p, st);
   }
   if (LOGN <= 11) {  // TK_FILTER_ALGO=warp: warp-per-row-pair variant (measured slower at cfg4)

@@ -395,9 +395,16 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     assert rel(got, want) < TOL
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "coef", "ldg", "tex"])
-def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
+def _set_bp_algo(monkeypatch, algo):
+    if algo == "quad8x1":  # quad kernel with the 8x1 quarter-warp voxel mapping
+        monkeypatch.setenv("TK_BP_Q42", "0")
+        algo = "quad"
     monkeypatch.setenv("TK_BP_ALGO", algo)
+
+
+@pytest.mark.parametrize("algo", ["smem", "quad", "quad8x1", "coef", "ldg", "tex"])
+def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
+    _set_bp_algo(monkeypatch, algo)
     geom = cone(tk, 24, 36, 1.5, 19)
     y = np.random.default_rng(22).standard_normal((19, 36, 36))
     for w in (False, True):
@@ -409,11 +416,11 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "coef", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["smem", "quad", "quad8x1", "coef", "ldg", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
-    monkeypatch.setenv("TK_BP_ALGO", algo)
+    _set_bp_algo(monkeypatch, algo)
     from paper_2511_08427_b200 import distributed as D
     from paper_2511_08427_b200.projectors import bp_cone_tensor_ex
 
