@@ -125,7 +125,7 @@ def measured_peaks():
 
 
 FP_KERNEL = "cone_fp4_kernel"  # the default forward projector (TK_FP_ALGO=ldg4m: <.., true>)
-BP_KERNEL = "cone_bp_quad_kernel"  # the default back projector (TK_BP_ALGO=quad)
+BP_KERNEL = "cone_bp_tma_kernel"  # the default back projector (TK_BP_ALGO=tma)
 
 
 def ncu_traffic():

@@ -1,0 +1,338 @@
+// tk_bp_tma.cu -- TMA-staged voxel-driven cone back projector for sm_100a
+// ("tma", default for z-invariant trajectories when the detector width is a
+// multiple of 4).  Semantics: reference _kernels.py:281-322 (back_cone_3d).
+//
+// Why: the quad-gather back projector (tk_cone.cu) is bound by the L1 LSU
+// data pipe -- every 16-byte quad load costs one wavefront per 128-byte line
+// touched by each quarter-warp (~1.4 lines per quarter at cfg4, ncu), and the
+// quad layout itself is a 12 GB expansion written every call.  Here
+//   * a CTA owns a 16 x 16 x 16 voxel block; for every view a producer warp
+//     projects the block's 8 corners (exact bound of a central projection of a
+//     convex box), and one elected lane issues ONE 3D TMA copy of the covering
+//     detector rectangle [r0, r0 + bh) x [c0, c0 + bw) of that view (c0 a
+//     multiple of 4: TMA box starts must be 16-byte aligned) into a
+//     shared-memory stage (out-of-detector texels are zero-filled by the TMA
+//     unit: the reference's per-tap zero extension, _kernels.py:308-317);
+//   * an 8-stage mbarrier ring (full: TMA bytes landed, empty: the 8 consumer
+//     warps are done) keeps 7 views in flight while 256 consumer threads
+//     (one (x, y) column and 16 z-voxels each) gather the 4 bilinear taps of
+//     every update with scalar LDS -- one data-pipe wavefront per warp and tap,
+//     conflict-light because a warp's footprint is ~20 consecutive columns;
+//   * column, depth and (sid/w)^2 are computed once per (column, view); only the
+//     row advances along z; floors use floor_magic (no conversion-pipe ops).
+// A (block, view) whose rectangle exceeds the TMA box (extreme magnification)
+// or that reaches behind the source is gathered from global memory with the
+// reference's per-tap bounds instead.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "tk_cone_bp.cuh"
+
+namespace tk {
+
+constexpr int kBtTX = 16, kBtTY = 16, kBtZB = 16, kBtStages = 8;
+constexpr int kBtConsumers = kBtTX * kBtTY;       // 8 warps
+constexpr int kBtThreads = kBtConsumers + 32;     // + 1 producer warp
+
+struct BtMeta {
+  int c0, r0, fits, pad;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c, int r, int v,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(v), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(kBtThreads, 2)
+    cone_bp_tma_kernel(const __grid_constant__ CUtensorMap map, const BpParams p, int bw, int bh,
+                       int stage_floats) {
+  extern __shared__ float bt_raw[];  // [kBtStages][stage_floats] at a 128-byte aligned base
+  // align by an element offset (not through uintptr_t) so the compiler keeps
+  // the pointer in the shared window: LDS with 32-bit addresses, not generic LD
+  float *bt_tiles = bt_raw + (((128u - (smem_u32(bt_raw) & 127u)) & 127u) >> 2);
+  __shared__ __align__(8) uint64_t full[kBtStages], empty[kBtStages];
+  __shared__ BtMeta meta[kBtStages];
+  __shared__ ConeVoxView sviews[kBtStages];  // the stage's view constants, written by the producer
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kBtStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBtConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int zl0 = blockIdx.z * kBtZB;
+
+  if (warp == kBtConsumers / 32) {  // ---------------- producer warp ----------------
+    // the block's voxel-centre box in centred index units (clipped to the volume)
+    const float bx0 = (float)(blockIdx.x * kBtTX) - p.cx;
+    const float bx1 = (float)(min((int)(blockIdx.x + 1) * kBtTX, p.nx) - 1) - p.cx;
+    const float by0 = (float)(blockIdx.y * kBtTY) - p.cy;
+    const float by1 = (float)(min((int)(blockIdx.y + 1) * kBtTY, p.ny) - 1) - p.cy;
+    const float bz0 = (float)(p.z_begin + zl0) - p.cz;
+    const float bz1 = bz0 + (float)(kBtZB - 1);  // consumers evaluate all kBtZB rows (stores are masked)
+    const unsigned tx_bytes = (unsigned)(bw * bh * 4);
+    for (int v = 0; v < p.n_views; ++v) {
+      const int s = v % kBtStages;
+      if (v >= kBtStages) mbar_wait(&empty[s], (unsigned)((v / kBtStages - 1) & 1));
+      const ConeVoxView &V = p.views[v];
+      float cmin = 3e38f, cmax = -3e38f, rmin = 3e38f, rmax = -3e38f;
+      bool behind = false;
+      if (lane < 8) {
+        const float x = (lane & 1) ? bx1 : bx0, y = (lane & 2) ? by1 : by0, z = (lane & 4) ? bz1 : bz0;
+        const float w = fmaf(V.w[0], x, fmaf(V.w[1], y, fmaf(V.w[2], z, V.w[3])));
+        behind = !(w > (float)kTiny);
+        const float rw = 1.f / w;
+        const float fc = fmaf(fmaf(V.a[0], x, fmaf(V.a[1], y, fmaf(V.a[2], z, V.a[3]))), rw, p.cu);
+        const float fr = fmaf(fmaf(V.b[0], x, fmaf(V.b[1], y, fmaf(V.b[2], z, V.b[3]))), rw, p.cv);
+        cmin = cmax = fc;
+        rmin = rmax = fr;
+      }
+#pragma unroll
+      for (int o = 4; o >= 1; o >>= 1) {
+        cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+        cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+        rmin = fminf(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+        rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      }
+      behind = __any_sync(0xffffffffu, behind);
+      if (lane == 0) {
+        BtMeta m;
+        bool fits = !behind && cmax - cmin < 1e6f && rmax - rmin < 1e6f && cmin > -1e6f &&
+                    cmax < 1e6f && rmin > -1e6f && rmax < 1e6f;
+        // taps floor(f) and floor(f) + 1, one texel of rounding margin each side
+        // the box's innermost start must be 16-byte aligned (TMA faults otherwise): c0 % 4 == 0
+        m.c0 = fits ? (((int)floorf(cmin) - 1) & ~3) : 0;
+        m.r0 = fits ? (int)floorf(rmin) - 1 : 0;
+        fits = fits && (int)floorf(cmax) + 3 - m.c0 <= bw && (int)floorf(rmax) + 3 - m.r0 <= bh;
+        m.fits = fits ? 1 : 0;
+        m.pad = 0;
+        meta[s] = m;
+        sviews[s] = V;
+        if (fits) {
+          mbar_arrive_tx(&full[s], tx_bytes);
+          tma_load_3d(bt_tiles + (size_t)s * stage_floats, &map, m.c0, m.r0, v, &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---------------- consumer warps: one (x, y) column x kBtZB z-voxels per thread ----------------
+  const int ix = blockIdx.x * kBtTX + (tid & (kBtTX - 1));
+  const int iy = blockIdx.y * kBtTY + tid / kBtTX;
+  const bool active = ix < p.nx && iy < p.ny;
+  const float xc = (float)ix - p.cx, yc = (float)iy - p.cy;
+  const float zc0 = (float)(p.z_begin + zl0) - p.cz;
+  float acc[kBtZB];
+#pragma unroll
+  for (int k = 0; k < kBtZB; ++k) acc[k] = 0.f;
+
+  for (int v = 0; v < p.n_views; ++v) {
+    const int s = v % kBtStages;
+    mbar_wait(&full[s], (unsigned)((v / kBtStages) & 1));
+    const BtMeta m = meta[s];
+    const ConeVoxView &V = sviews[s];
+    const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
+    const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
+    const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+    if (active && w0 > (float)kTiny) {  // _kernels.py:297-298
+      const float rw = 1.f / w0;
+      const float fc = fmaf(a0, rw, p.cu);
+      const float xcf = floor_magic(fc);
+      const float wc = fc - (xcf - kFloorMagic);
+      float q = 1.f;
+      if (WEIGHTED) {  // (sid / w)^2, _kernels.py:318-320
+        q = p.sid * rw;
+        q *= q;
+      }
+      const float g0 = q * (1.f - wc), g1 = q * wc;
+      const float fr0 = fmaf(b0, rw, p.cv);
+      const float dr = V.b[2] * rw;
+      if (m.fits) {
+        const float *t = bt_tiles + (size_t)s * stage_floats +
+                         ((int)(__float_as_uint(xcf) - kFloorBits) - m.c0);
+        const int rbias = (int)kFloorBits + m.r0;
+#pragma unroll
+        for (int k = 0; k < kBtZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float xr = floor_magic(fr);
+          const float *e = t + ((int)__float_as_uint(xr) - rbias) * bw;
+          const float top = fmaf(g1, e[1], g0 * e[0]);
+          const float bot = fmaf(g1, e[bw + 1], g0 * e[bw]);
+          acc[k] += fmaf(fr - (xr - kFloorMagic), bot - top, top);
+        }
+      } else {  // rectangle exceeds the TMA box: bounded global gathers
+        const float *sv = p.sino + (long long)v * p.view_stride;
+        const int c0 = (int)(__float_as_uint(xcf) - kFloorBits);
+        const bool ca = (unsigned)c0 < (unsigned)p.cols, cb = (unsigned)(c0 + 1) < (unsigned)p.cols;
+#pragma unroll
+        for (int k = 0; k < kBtZB; ++k) {
+          const float fr = fmaf((float)k, dr, fr0);
+          const float flr = floorf(fr);
+          const int r0 = (int)flr;
+          const bool ra = (unsigned)r0 < (unsigned)p.band_rows;
+          const bool rb = (unsigned)(r0 + 1) < (unsigned)p.band_rows;
+          const float *e = sv + (long long)r0 * p.cols + c0;
+          const float t00 = (ra && ca) ? __ldg(e) : 0.f, t01 = (ra && cb) ? __ldg(e + 1) : 0.f;
+          const float t10 = (rb && ca) ? __ldg(e + p.cols) : 0.f;
+          const float t11 = (rb && cb) ? __ldg(e + p.cols + 1) : 0.f;
+          const float top = fmaf(g1, t01, g0 * t00);
+          const float bot = fmaf(g1, t11, g0 * t10);
+          acc[k] += fmaf(fr - flr, bot - top, top);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < kBtZB; ++k) {
+    const int zl = zl0 + k;
+    if (zl < p.z_count) {
+      float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
+      *o = p.accumulate ? *o + acc[k] : acc[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// Detector rectangle (columns, rows) a 16^3 block needs in the worst sampled
+// (block, view): volume-shell and interior blocks x up to 24 views.  Blocks or
+// views outside the sample that need more fall back to global gathers in-kernel.
+static void footprint_box(const BpParams &p, const ConeVoxView *hv, int &bw, int &bh) {
+  const int nbx = (p.nx + kBtTX - 1) / kBtTX, nby = (p.ny + kBtTY - 1) / kBtTY;
+  const int nbz = (p.z_count + kBtZB - 1) / kBtZB;
+  auto picks = [](int n) {
+    std::vector<int> v = {0, 1, n / 4, n / 2, (3 * n) / 4, n - 2, n - 1};
+    std::vector<int> out;
+    for (int x : v)
+      if (x >= 0 && x < n && std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+    return out;
+  };
+  const std::vector<int> px = picks(nbx), py = picks(nby), pz = picks(nbz);
+  const int nv = std::min(p.n_views, 24);
+  int wmax = 2, hmax = 2;
+  for (int iv = 0; iv < nv; ++iv) {
+    const ConeVoxView &V = hv[(long long)iv * p.n_views / nv];
+    for (int bx : px)
+      for (int by : py)
+        for (int bz : pz) {
+          const double x0 = bx * kBtTX - (double)p.cx, x1 = std::min((bx + 1) * kBtTX, p.nx) - 1 - (double)p.cx;
+          const double y0 = by * kBtTY - (double)p.cy, y1 = std::min((by + 1) * kBtTY, p.ny) - 1 - (double)p.cy;
+          const double z0 = p.z_begin + bz * kBtZB - (double)p.cz;
+          const double z1 = z0 + (kBtZB - 1);
+          double cmin = 1e300, cmax = -1e300, rmin = 1e300, rmax = -1e300;
+          bool ok = true;
+          for (int i = 0; i < 8; ++i) {
+            const double x = (i & 1) ? x1 : x0, y = (i & 2) ? y1 : y0, z = (i & 4) ? z1 : z0;
+            const double w = V.w[0] * x + V.w[1] * y + V.w[2] * z + V.w[3];
+            if (!(w > 1e-12)) {
+              ok = false;
+              break;
+            }
+            const double fc = (V.a[0] * x + V.a[1] * y + V.a[2] * z + V.a[3]) / w + p.cu;
+            const double fr = (V.b[0] * x + V.b[1] * y + V.b[2] * z + V.b[3]) / w + p.cv;
+            cmin = std::min(cmin, fc), cmax = std::max(cmax, fc);
+            rmin = std::min(rmin, fr), rmax = std::max(rmax, fr);
+          }
+          if (!ok || cmax - cmin > 4096 || rmax - rmin > 4096) continue;
+          wmax = std::max(wmax, (int)std::floor(cmax) + 3 - ((int)std::floor(cmin) - 1));
+          hmax = std::max(hmax, (int)std::floor(rmax) + 3 - ((int)std::floor(rmin) - 1));
+        }
+  }
+  bw = ((wmax + 3 + 2 + 3) / 4) * 4;  // +3 for the 16-byte aligned start column, +2 slack
+  // row pitch = 24..28 (mod 32) words: a warp's lanes sit in one or two adjacent
+  // detector rows ~20 columns wide, so lanes one row apart collide on a bank only
+  // for column offsets >= 24
+  while (bw % 32 < 24 || bw % 32 > 28) bw += 4;
+  bh = hmax + 2;
+}
+
+int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighted, cudaStream_t st) {
+  auto enc = encode_fn();
+  if (!enc) return -1;
+  if (p.cols % 4 != 0 || (reinterpret_cast<uintptr_t>(p.sino) & 15) != 0) return -1;
+  if (p.view_stride != (long long)p.band_rows * p.cols) return -1;
+  int bw = 0, bh = 0;
+  footprint_box(p, host_views, bw, bh);
+  if (bw > 256 || bh > 256) return -1;
+  const int stage_floats = ((bw * bh + 31) / 32) * 32;  // 128-byte aligned stages
+  const size_t smem = sizeof(float) * (size_t)stage_floats * kBtStages + 128;
+  if (smem > 200 * 1024) return -1;
+
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)p.cols, (cuuint64_t)p.band_rows, (cuuint64_t)p.n_views};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.cols * 4, (cuuint64_t)p.band_rows * p.cols * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(p.sino), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -1;
+  auto kern = weighted ? cone_bp_tma_kernel<true> : cone_bp_tma_kernel<false>;
+  TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + kBtZB - 1) / kBtZB);
+  kern<<<grid, kBtThreads, smem, st>>>(map, p, bw, bh, stage_floats);
+  TK_LAUNCHED("cone_bp_tma_kernel");
+  return TK_OK;
+}
+
+}  // namespace tk

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "tk_common.cuh"
+#include "tk_cone_bp.cuh"
 #include "tk_tex.cuh"
 
 namespace tk {
@@ -31,11 +32,6 @@ struct ConeRayView {  // per-view forward constants (float64): source, M^-1
   double minv[9];
 };
 
-struct ConeVoxView {  // per-view back constants (float32), see pack_bp_views
-  float a[4];  // column numerator (principal-point shifted)
-  float b[4];  // row numerator (principal-point shifted)
-  float w[4];  // depth
-};
 
 // ---------------------------------------------------------------------------
 // zero-padded copy: volp (nz+2, ny+2, nx+2)  <-  vol (nz, ny, nx)
@@ -802,19 +798,6 @@ __global__ void __launch_bounds__(kFpBX *kFpBY)
 // ---------------------------------------------------------------------------
 constexpr int kBpBX = 32, kBpBY = 8, kBpChunk = 128;
 
-struct BpParams {
-  const float *sino;
-  long long view_stride;  // elements between views of the (band) sinogram
-  int n_views, band_rows, cols;
-  const ConeVoxView *views;
-  float cu, cv;  // column / row shift constants (cv already minus row_begin)
-  float sid;
-  int nx, ny, z_begin, z_count;
-  float cx, cy, cz;  // volume centre (index units)
-  int accumulate;
-  float *out;
-  cudaTextureObject_t tex;  // layered sinogram (texture variants only)
-};
 
 // Column taps (clamped indices + weights, zero outside [0, cols)).
 __device__ __forceinline__ void col_taps(float fc, int cols, int &ca, int &cb, float &g0,
@@ -1809,17 +1792,20 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   return TK_OK;
 }
 
-// Back-projector algorithm: TK_BP_ALGO = quad (default) | coef | smem | ldg | tex | hwtex.
-enum class BpAlgo { kCoef, kSmem, kQuad, kLdg, kTex, kHwTex };
+// Back-projector algorithm: TK_BP_ALGO = tma (default) | quad | coef | smem | ldg | tex | hwtex.
+// tma needs a z-invariant trajectory and a detector width that is a multiple of
+// 4 (16-byte TMA row pitch); otherwise quad runs.
+enum class BpAlgo { kTma, kCoef, kSmem, kQuad, kLdg, kTex, kHwTex };
 
 static BpAlgo bp_algo() {
   const char *e = getenv("TK_BP_ALGO");
+  if (e && !strcmp(e, "quad")) return BpAlgo::kQuad;
   if (e && !strcmp(e, "coef")) return BpAlgo::kCoef;
   if (e && !strcmp(e, "smem")) return BpAlgo::kSmem;
   if (e && !strcmp(e, "ldg")) return BpAlgo::kLdg;
   if (e && !strcmp(e, "tex")) return BpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return BpAlgo::kHwTex;
-  return BpAlgo::kQuad;
+  return BpAlgo::kTma;
 }
 
 constexpr int kBqZB = 16;
@@ -2015,6 +2001,11 @@ int tk_back_cone_3d_ex(const float *sino, int n_views, int rows, int cols, int r
   p.tex = 0;
   BpAlgo algo = bp_algo();
   if (algo == BpAlgo::kSmem && zinv) return launch_bp_smem(p, weighted != 0, st);
+  if (algo == BpAlgo::kTma && zinv) {
+    const int rc = launch_bp_tma(p, hv.data(), weighted != 0, st);
+    if (rc != -1) return rc;
+  }
+  if (algo == BpAlgo::kTma) algo = BpAlgo::kQuad;
   if (algo == BpAlgo::kCoef || algo == BpAlgo::kQuad || algo == BpAlgo::kSmem)
     return launch_bp_quad(p, weighted != 0, zinv, algo == BpAlgo::kCoef, st);
   if (n_views > 2048) algo = BpAlgo::kLdg;  // layered arrays hold <= 2048 layers

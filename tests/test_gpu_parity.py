@@ -402,7 +402,7 @@ def _set_bp_algo(monkeypatch, algo):
     monkeypatch.setenv("TK_BP_ALGO", algo)
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "quad8x1", "coef", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["tma", "smem", "quad", "quad8x1", "coef", "ldg", "tex"])
 def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     _set_bp_algo(monkeypatch, algo)
     geom = cone(tk, 24, 36, 1.5, 19)
@@ -416,7 +416,7 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["smem", "quad", "quad8x1", "coef", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["tma", "smem", "quad", "quad8x1", "coef", "ldg", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
@@ -436,11 +436,12 @@ def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
             assert rel(slab, full[z0:z1].cpu().numpy()) < 1e-5  # fp32 row-shift rounding
 
 
+@pytest.mark.parametrize("algo", ["smem", "tma"])
 @pytest.mark.parametrize("det_pitch", [0.05, 0.4, 3.0])
-def test_bp_smem_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch):
+def test_bp_smem_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch, algo):
     """Fine detector pitch makes the CTA footprint exceed the shared-memory tile
     (global-gather fallback); coarse pitch makes whole volumes fit one tile."""
-    monkeypatch.setenv("TK_BP_ALGO", "smem")
+    monkeypatch.setenv("TK_BP_ALGO", algo)
     geom = tk.circular_cone_geometry((20, 36, 33), (1.0, 0.8, 1.2), (40, 50), (det_pitch, det_pitch), 7,
                                      2 * np.pi, 1200.0, 750.0)
     y = np.random.default_rng(23).standard_normal((7, 40, 50))
@@ -554,3 +555,18 @@ def test_filter_variants_match_oracle(tk, oracle, monkeypatch, algo, cols, rows,
     if rows > 2:  # band of detector rows [1, rows-1) with the global row offset
         band = filter_stage_tensor(T(y[:, 1:rows - 1]).contiguous(), geom, "shepp_logan", row_offset=1)
         assert rel(band, want[:, 1:rows - 1]) < TOL
+
+
+@pytest.mark.parametrize("cols", [64, 66])
+def test_bp_tma_large_volume_edges(tk, oracle, monkeypatch, cols):
+    """TMA-staged back projection on a volume whose blocks reach the detector
+    edges (out-of-detector texels zero-filled by the TMA unit) and a partial
+    last block in every axis; cols = 66 takes the quad fallback (16-byte row pitch)."""
+    monkeypatch.setenv("TK_BP_ALGO", "tma")
+    geom = tk.circular_cone_geometry((37, 45, 41), (1.1, 1.0, 0.9), (40, cols), (1.3, 1.2), 23, 2 * np.pi,
+                                     1200.0, 750.0)
+    y = np.random.default_rng(cols).standard_normal((23, 40, cols))
+    for w in (False, True):
+        got = tk.back_project(tk.Sinogram(y, (1.3, 1.2)), geom, w).data
+        want = oracle.back_cone_3d(y, geom.matrix_array(), 750.0, (37, 45, 41), (1.1, 1.0, 0.9), w)
+        assert rel(got, want) < TOL
