@@ -86,7 +86,6 @@ __global__ void __launch_bounds__(kBtThreads, 2)
   float *bt_tiles = bt_raw + (((128u - (smem_u32(bt_raw) & 127u)) & 127u) >> 2);
   __shared__ __align__(8) uint64_t full[kBtStages], empty[kBtStages];
   __shared__ BtMeta meta[kBtStages];
-  __shared__ ConeVoxView sviews[kBtStages];  // the stage's view constants, written by the producer
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -144,7 +143,6 @@ __global__ void __launch_bounds__(kBtThreads, 2)
         m.fits = fits ? 1 : 0;
         m.pad = 0;
         meta[s] = m;
-        sviews[s] = V;
         if (fits) {
           mbar_arrive_tx(&full[s], tx_bytes);
           tma_load_3d(bt_tiles + (size_t)s * stage_floats, &map, m.c0, m.r0, v, &full[s]);
@@ -171,7 +169,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     const int s = v % kBtStages;
     mbar_wait(&full[s], (unsigned)((v / kBtStages) & 1));
     const BtMeta m = meta[s];
-    const ConeVoxView &V = sviews[s];
+    const ConeVoxView &V = p.views[v];  // uniform across the CTA: L1 broadcast (measured faster than a smem copy)
     const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
     const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
     const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
@@ -299,10 +297,7 @@ static void footprint_box(const BpParams &p, const ConeVoxView *hv, int &bw, int
         }
   }
   bw = ((wmax + 3 + 2 + 3) / 4) * 4;  // +3 for the 16-byte aligned start column, +2 slack
-  // row pitch = 24..28 (mod 32) words: a warp's lanes sit in one or two adjacent
-  // detector rows ~20 columns wide, so lanes one row apart collide on a bank only
-  // for column offsets >= 24
-  while (bw % 32 < 24 || bw % 32 > 28) bw += 4;
+  if (bw % 32 == 0) bw += 4;  // row pitch off the 32-bank period (a pitch of 24..28 mod 32 measured no better)
   bh = hmax + 2;
 }
 

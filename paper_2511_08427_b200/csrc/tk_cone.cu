@@ -336,8 +336,11 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
 // so a cell is 2 LDG.128 (slices z and z+1) instead of 8 LDG.32.
 // Same traversal, ordering, arithmetic order of weights as cone_fp2_kernel.
 // ---------------------------------------------------------------------------
+// diff = 1 stores (v00, v01 - v00, v10, v11 - v10) (fast-axis differences
+// pre-subtracted: the sample's fast-axis lerps become single FFMAs with the same
+// fp32 rounding as fmaf(w, b - a, a), i.e. bit-identical results).
 __global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
-                                   float4 *__restrict__ q) {
+                                   float4 *__restrict__ q, int diff = 0) {
   constexpr int m = kFpMargin;
   const int na = swap_xy ? ny : nx, nb = swap_xy ? nx : ny;
   const int pa = na + 2 * m, pb = nb + 2 * m, pz = nz + 2 * m;
@@ -359,7 +362,7 @@ __global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny
       }
       v[j] = val;
     }
-    q[i] = make_float4(v[0], v[1], v[2], v[3]);
+    q[i] = diff ? make_float4(v[0], v[1] - v[0], v[2], v[3] - v[2]) : make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -427,6 +430,11 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
       hi4 = __ldg(p + ps);
     }
     const float wa = fa - la, wb = fb - lb;
+    if (MAGIC) {  // difference quads (quad_volume_kernel diff = 1)
+      const float s0 = lerpf(fmaf(wa, lo4.y, lo4.x), fmaf(wa, lo4.w, lo4.z), wb);
+      const float s1 = lerpf(fmaf(wa, hi4.y, hi4.x), fmaf(wa, hi4.w, hi4.z), wb);
+      return lerpf(s0, s1, fz - lz);
+    }
     const float s0 = lerpf(lerpf(lo4.x, lo4.y, wa), lerpf(lo4.z, lo4.w, wa), wb);
     const float s1 = lerpf(lerpf(hi4.x, hi4.y, wa), lerpf(hi4.z, hi4.w, wa), wb);
     return lerpf(s0, s1, fz - lz);
@@ -1598,7 +1606,8 @@ static FpAlgo fp_algo() {
 struct FpPlan {
   int nz, ny, nx;
   double sz, sy, sx;
-  bool coef = true;  // Cell8 (ldg8) or float4 quads (ldg4)
+  bool coef = true;   // Cell8 (ldg8) or float4 quads (ldg4 / ldg4m)
+  bool diff = false;  // difference quads (ldg4m)
   void *qA = nullptr, *qB = nullptr;
 };
 
@@ -1611,6 +1620,7 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->sy = sy;
   plan->sx = sx;
   plan->coef = fp_algo() == FpAlgo::kLdg8;
+  plan->diff = fp_algo() == FpAlgo::kLdg4m;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
@@ -1623,7 +1633,8 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       coef_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<Cell8 *>(dst));
       TK_LAUNCHED("coef_volume_kernel");
     } else {
-      quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst));
+      quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst),
+                                                plan->diff ? 1 : 0);
       TK_LAUNCHED("quad_volume_kernel");
     }
   }
@@ -1665,7 +1676,7 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
   } else {
-    const bool magic = fp_algo() == FpAlgo::kLdg4m;
+    const bool magic = pl.diff;  // ldg4m: FADD.RM floors + difference quads
     auto kern = minb >= 12 ? (magic ? cone_fp4_kernel<12, true> : cone_fp4_kernel<12, false>)
                            : (magic ? cone_fp4_kernel<10, true> : cone_fp4_kernel<10, false>);
     if (magic && wr == 4) kern = cone_fp4_kernel<12, true, 4>;

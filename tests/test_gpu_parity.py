@@ -452,7 +452,9 @@ def test_bp_smem_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch, alg
 
 def test_overlapped_host_pipeline_matches_device(tk):
     """Pinned-host boundary calls (chunked plan projection with overlapped D2H,
-    chunked H2D + filtering) equal the device-resident operators bit for bit."""
+    chunked H2D + filtering + accumulating back projection) equal the
+    device-resident operators (bit for bit for the projection; to summation
+    order for the chunked FDK)."""
     from paper_2511_08427_b200 import ops
     from paper_2511_08427_b200.filters import fdk_tensor
     from paper_2511_08427_b200.projectors import ForwardProjectionPlan, fp_tensor
@@ -469,8 +471,8 @@ def test_overlapped_host_pipeline_matches_device(tk):
         part = torch.empty(10, 50, 60, device="cuda")
         plan.project(slice(5, 15), part, 0.5)
         assert torch.equal(part, want[5:15])
-    rec = ops.py_fbp(got, cfg)
-    assert rec.is_pinned() and torch.allclose(rec, fdk_tensor(want, geom, "cosine").cpu(), rtol=0, atol=1e-6)
+    rec = ops.py_fbp(got, cfg)  # view-chunked filter + accumulating back projection
+    assert rec.is_pinned() and rel(rec, fdk_tensor(want, geom, "cosine")) < 1e-6
 
 
 def test_grid_files_roundtrip_and_reference_format(tk, tmp_path, golden):
