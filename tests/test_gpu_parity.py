@@ -472,7 +472,7 @@ def test_overlapped_host_pipeline_matches_device(tk):
         plan.project(slice(5, 15), part, 0.5)
         assert torch.equal(part, want[5:15])
     rec = ops.py_fbp(got, cfg)  # view-chunked filter + accumulating back projection
-    assert rec.is_pinned() and rel(rec, fdk_tensor(want, geom, "cosine")) < 1e-6
+    assert rec.is_pinned() and rel(rec, fdk_tensor(want, geom, "cosine").cpu()) < 1e-6
 
 
 def test_grid_files_roundtrip_and_reference_format(tk, tmp_path, golden):
