@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
 }
 
 // ---------------------------------------------------------------------------
-// Forward projection, coefficient-cell variant ("ldg8", default).
+// Forward projection, coefficient-cell variant ("ldg8").
 //
 // The ncu capture of cone_fp4_kernel (profiles/ncu_r01c_*) shows an issue-
 // bound loop of ~42 instructions per sample, 5 of them conversions (3 FRND
