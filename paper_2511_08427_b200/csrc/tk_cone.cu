@@ -449,6 +449,110 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Forward projection, b-plane quad variant ("ldg4p").
+//
+// Rays travel mostly along the middle axis b (the orientation copy puts the
+// detector u direction on the fast axis a).  Here the taps are grouped per
+// b-plane: Qp[b][z][a] = (V[z][b][a], V[z][b][a+1] - V[z][b][a],
+// V[z+1][b][a], V[z+1][b][a+1] - V[z+1][b][a]), and a lane holds the two planes
+// of its cell as "near" and "far" along its direction of travel.  A step into
+// the next cell along b with the same (a, z) -- the most frequent change --
+// keeps far as the new near and loads only the new far plane, so the "near"
+// load is issued by far fewer lanes of each quarter-warp and touches fewer
+// 128-byte lines (L1 data-pipe wavefronts; a trace of the cfg4
+// access pattern predicts -21 % wavefronts per sample).
+// ---------------------------------------------------------------------------
+__global__ void plane_quad_volume_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
+                                         float4 *__restrict__ q) {
+  constexpr int m = kFpMargin;
+  const int na = swap_xy ? ny : nx, nb = swap_xy ? nx : ny;
+  const int pa = na + 2 * m, pb = nb + 2 * m, pz = nz + 2 * m;
+  const long long total = (long long)pb * pz * pa;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(i % pa) - m;
+    const long long t = i / pa;
+    const int z = (int)(t % pz) - m;
+    const int b = (int)(t / pz) - m;
+    float v[4];  // v[dz * 2 + da]
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int aa = a + (j & 1), zz = z + (j >> 1);
+      float val = 0.f;
+      if ((unsigned)zz < (unsigned)nz && (unsigned)aa < (unsigned)na && (unsigned)b < (unsigned)nb) {
+        const int x = swap_xy ? b : aa, y = swap_xy ? aa : b;
+        val = __ldg(vol + ((long long)zz * ny + y) * nx + x);
+      }
+      v[j] = val;
+    }
+    q[i] = make_float4(v[0], v[1] - v[0], v[2], v[3] - v[2]);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
+    cone_fp4p_kernel(const float4 *__restrict__ qA, const float4 *__restrict__ qB, int nx, int ny,
+                     int nz, double sx, double sy, double sz, const Fp2View *__restrict__ views,
+                     int rows, int cols, int n_views, double step, float *__restrict__ out) {
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r = rb * kFp2BY + threadIdx.y;
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  const float4 *q = W.swap ? qB : qA;
+  const int na = W.swap ? ny : nx;
+  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const unsigned pa = (unsigned)(na + 2 * kFpMargin);
+  const unsigned pp = (unsigned)(nz + 2 * kFpMargin) * pa;  // b-plane stride
+  const unsigned bias = kFloorBits * (1u + pa + pp);
+  const bool fwd = gb >= 0.f;                      // direction of travel along b
+  const unsigned far_off = fwd ? pp : 0u, near_off = fwd ? 0u : pp;
+  const unsigned bstep = fwd ? pp : 0u - pp;        // cell index change of a pure b step
+  const float tsgn = fwd ? 1.f : -1.f, toff = fwd ? 0.f : 1.f;  // weight of far: wb or 1 - wb
+  unsigned cell = 0x80000000u;
+  float4 nr = make_float4(0.f, 0.f, 0.f, 0.f), fr = nr;
+  auto sample = [&](float kk) -> float {
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xb) * pp + (__float_as_uint(xz) * pa + __float_as_uint(xa)) - bias;
+    if (id != cell) {
+      if (id - cell == bstep) {
+        nr = fr;
+      } else {
+        nr = __ldg(elem_ptr(q, id + near_off));
+      }
+      fr = __ldg(elem_ptr(q, id + far_off));
+      cell = id;
+    }
+    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float sn = lerpf(fmaf(wa, nr.y, nr.x), fmaf(wa, nr.w, nr.z), wz);
+    const float sf = lerpf(fmaf(wa, fr.y, fr.x), fmaf(wa, fr.w, fr.z), wz);
+    return lerpf(sn, sf, fmaf(tsgn, wb, toff));
+  };
+  float acc = 0.f;
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+#pragma unroll 2
+  for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+  acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
+  *dst = acc * (float)step;
+}
+
+// ---------------------------------------------------------------------------
 // Forward projection, coefficient-cell variant ("ldg8").
 //
 // The ncu capture of cone_fp4_kernel (profiles/ncu_r01c_*) shows an issue-
@@ -1585,8 +1689,8 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg4m (default) | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
-enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg4m (default) | ldg4p | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg4p, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
@@ -1596,6 +1700,7 @@ static FpAlgo fp_algo() {
   if (e && !strcmp(e, "tex")) return FpAlgo::kTex;
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
   if (e && !strcmp(e, "ldg8")) return FpAlgo::kLdg8;
+  if (e && !strcmp(e, "ldg4p")) return FpAlgo::kLdg4p;
   return FpAlgo::kLdg4m;
 }
 
@@ -1608,6 +1713,7 @@ struct FpPlan {
   double sz, sy, sx;
   bool coef = true;   // Cell8 (ldg8) or float4 quads (ldg4 / ldg4m)
   bool diff = false;  // difference quads (ldg4m)
+  bool plane = false; // b-plane difference quads (ldg4p)
   void *qA = nullptr, *qB = nullptr;
 };
 
@@ -1621,6 +1727,7 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->sx = sx;
   plan->coef = fp_algo() == FpAlgo::kLdg8;
   plan->diff = fp_algo() == FpAlgo::kLdg4m;
+  plan->plane = fp_algo() == FpAlgo::kLdg4p;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
@@ -1632,6 +1739,9 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
     if (plan->coef) {
       coef_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<Cell8 *>(dst));
       TK_LAUNCHED("coef_volume_kernel");
+    } else if (plan->plane) {
+      plane_quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst));
+      TK_LAUNCHED("plane_quad_volume_kernel");
     } else {
       quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst),
                                                 plan->diff ? 1 : 0);
@@ -1675,6 +1785,12 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
+  } else if (pl.plane) {
+    auto kern = minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;
+    kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const float4 *>(pl.qA), static_cast<const float4 *>(pl.qB),
+                                              pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
+                                              cols, n_views, step, out);
+    TK_LAUNCHED("cone_fp4p_kernel");
   } else {
     const bool magic = pl.diff;  // ldg4m: FADD.RM floors + difference quads
     auto kern = minb >= 12 ? (magic ? cone_fp4_kernel<12, true> : cone_fp4_kernel<12, false>)
@@ -1760,7 +1876,7 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
-  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m))
+  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m || algo == FpAlgo::kLdg4p))
     return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
