@@ -529,15 +529,13 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
     const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
     const unsigned id = __float_as_uint(xb) * pp + (__float_as_uint(xz) * pa + __float_as_uint(xa)) - bias;
-    if (id != cell) {
-      if (id - cell == bstep) {
-        nr = fr;
-      } else {
-        nr = __ldg(elem_ptr(q, id + near_off));
-      }
-      fr = __ldg(elem_ptr(q, id + far_off));
-      cell = id;
-    }
+    // straight-line, predicated: shift (near <- far) or reload near, then the new far
+    const bool chg = id != cell;
+    const bool sh = id - cell == bstep;  // implies chg
+    if (sh) nr = fr;
+    if (chg && !sh) nr = __ldg(elem_ptr(q, id + near_off));
+    if (chg) fr = __ldg(elem_ptr(q, id + far_off));
+    cell = id;
     const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
     const float sn = lerpf(fmaf(wa, nr.y, nr.x), fmaf(wa, nr.w, nr.z), wz);
     const float sf = lerpf(fmaf(wa, fr.y, fr.x), fmaf(wa, fr.w, fr.z), wz);
@@ -1786,7 +1784,7 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
   } else if (pl.plane) {
-    auto kern = minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;
+    auto kern = mb && minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;  // 10: no spills (measured best)
     kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const float4 *>(pl.qA), static_cast<const float4 *>(pl.qB),
                                               pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
                                               cols, n_views, step, out);
