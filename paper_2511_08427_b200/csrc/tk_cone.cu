@@ -23,15 +23,10 @@
 
 #include "tk_common.cuh"
 #include "tk_cone_bp.cuh"
+#include "tk_cone_fp.cuh"
 #include "tk_tex.cuh"
 
 namespace tk {
-
-struct ConeRayView {  // per-view forward constants (float64): source, M^-1
-  double src[3];
-  double minv[9];
-};
-
 
 // ---------------------------------------------------------------------------
 // zero-padded copy: volp (nz+2, ny+2, nx+2)  <-  vol (nz, ny, nx)
@@ -66,65 +61,6 @@ __global__ void crop3d_kernel(const float *__restrict__ volp, int nz, int ny, in
     int z = (int)(t / ny);
     vol[i] = volp[((long long)(z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + (x + 1)];
   }
-}
-
-// ---------------------------------------------------------------------------
-// Ray set-up shared by the forward projector and its transpose.
-// Returns false when the ray misses the box (reference _clip_ray_3d, t0 >= t1).
-// ---------------------------------------------------------------------------
-struct RaySetup {
-  float ex, ey, ez;  // padded-index coordinates of the clip entry point
-  float gx, gy, gz;  // padded-index increment per full step
-  int n;             // number of samples (reference loop count)
-  float last;        // fraction of a step covered by the last sample (0,1]
-};
-
-__device__ __forceinline__ bool clip_axis(double p, double d, double h, double &t0,
-                                          double &t1) {
-  if (fabs(d) > kTiny) {
-    double ta = (-h - p) / d, tb = (h - p) / d;
-    t0 = fmax(t0, fmin(ta, tb));
-    t1 = fmin(t1, fmax(ta, tb));
-    return true;
-  }
-  return !(p < -h || p > h);
-}
-
-__device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int c, int nx,
-                                               int ny, int nz, double sx, double sy,
-                                               double sz, double step, RaySetup &rs) {
-  // _kernels.py:262-265
-  double dx = V.minv[0] * c + V.minv[1] * r + V.minv[2];
-  double dy = V.minv[3] * c + V.minv[4] * r + V.minv[5];
-  double dz = V.minv[6] * c + V.minv[7] * r + V.minv[8];
-  double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
-  dx *= inv;
-  dy *= inv;
-  dz *= inv;
-  const double px = V.src[0], py = V.src[1], pz = V.src[2];
-  // _kernels.py:125-130 (_clip_ray_3d on the half-extents (n+1) s / 2)
-  double t0 = -1e300, t1 = 1e300;
-  if (!clip_axis(px, dx, (nx + 1) * sx / 2.0, t0, t1)) return false;
-  if (!clip_axis(py, dy, (ny + 1) * sy / 2.0, t0, t1)) return false;
-  if (!clip_axis(pz, dz, (nz + 1) * sz / 2.0, t0, t1)) return false;
-  if (!(t0 < t1)) return false;
-  // _kernels.py:133: while t < t1 - TINY  ->  n = ceil((t1 - TINY - t0) / step)
-  double span = (t1 - kTiny - t0) / step;
-  if (!(span > 0.0)) return false;
-  int n = (int)ceil(span);
-  double last = (t1 - t0) / step - (double)(n - 1);
-  if (last > 1.0) last = 1.0;
-  // padded-index coordinates (centre (n-1)/2 + 1, _kernels.py:122-124, 138-140)
-  const double cx = (nx - 1) / 2.0 + 1.0, cy = (ny - 1) / 2.0 + 1.0, cz = (nz - 1) / 2.0 + 1.0;
-  rs.ex = (float)((px + t0 * dx) / sx + cx);
-  rs.ey = (float)((py + t0 * dy) / sy + cy);
-  rs.ez = (float)((pz + t0 * dz) / sz + cz);
-  rs.gx = (float)(step * dx / sx);
-  rs.gy = (float)(step * dy / sy);
-  rs.gz = (float)(step * dz / sz);
-  rs.n = n;
-  rs.last = (float)last;
-  return true;
 }
 
 // One trilinear sample of the zero-padded volume at padded-index coordinates
@@ -202,7 +138,6 @@ __global__ void __launch_bounds__(kFpBX *kFpBY)
 //   half of them at step = s/2) issues no load.
 // ---------------------------------------------------------------------------
 constexpr int kFp2BX = 32, kFp2BY = 4;
-constexpr int kFpMargin = 2;
 
 // vol (nz, ny, nx) -> copy with a kFpMargin zero margin; swap_xy selects the
 // y-fastest orientation out[z][x][y].  Tiled through shared memory so both
@@ -233,12 +168,6 @@ __global__ void pad_margin_kernel(const float *__restrict__ vol, int nz, int ny,
     }
   }
 }
-
-struct Fp2View {
-  ConeRayView ray;
-  int swap;  // 1: use the y-fastest copy (x and y exchanged)
-  int pad;
-};
 
 struct CellTaps {  // the 8 taps of one cell: v[z][b][a], with d = v[..][1] - v[..][0]
   float v00, d00, v01, d01, v10, d10, v11, d11;
