@@ -36,7 +36,7 @@
 
 namespace tk {
 
-constexpr int kBtTX = 16, kBtTY = 16, kBtZB = 16, kBtStages = 8;
+constexpr int kBtTX = 16, kBtTY = 16, kBtMaxStages = 8;
 constexpr int kBtConsumers = kBtTX * kBtTY;       // 8 warps
 constexpr int kBtThreads = kBtConsumers + 32;     // + 1 producer warp
 
@@ -44,10 +44,13 @@ struct BtMeta {
   int c0, r0, fits, pad;
 };
 
-template <bool WEIGHTED>
+// ZB z-voxels per thread (16 or 32: 32 halves the per-view set-up per update),
+// NST stages in the mbarrier ring.
+template <bool WEIGHTED, int ZB, int NST>
 __global__ void __launch_bounds__(kBtThreads, 2)
     cone_bp_tma_kernel(const __grid_constant__ CUtensorMap map, const BpParams p, int bw, int bh,
                        int stage_floats) {
+  constexpr int kBtZB = ZB, kBtStages = NST;
   extern __shared__ float bt_raw[];  // [kBtStages][stage_floats] at a 128-byte aligned base
   // align by an element offset (not through uintptr_t) so the compiler keeps
   // the pointer in the shared window: LDS with 32-bit addresses, not generic LD
@@ -142,7 +145,8 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
     const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
     if (active && w0 > (float)kTiny) {  // _kernels.py:297-298
-      const float rw = 1.f / w0;
+      float rw;  // MUFU.RCP (rel. error 2^-23), one instruction instead of the IEEE division sequence
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"(w0));
       const float fc = fmaf(a0, rw, p.cu);
       const float xcf = floor_magic(fc);
       const float wc = fc - (xcf - kFloorMagic);
@@ -223,7 +227,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // Detector rectangle (columns, rows) a 16^3 block needs in the worst sampled
 // (block, view): volume-shell and interior blocks x up to 24 views.  Blocks or
 // views outside the sample that need more fall back to global gathers in-kernel.
-static void footprint_box(const BpParams &p, const ConeVoxView *hv, int &bw, int &bh) {
+static void footprint_box(const BpParams &p, const ConeVoxView *hv, int kBtZB, int &bw, int &bh) {
   const int nbx = (p.nx + kBtTX - 1) / kBtTX, nby = (p.ny + kBtTY - 1) / kBtTY;
   const int nbz = (p.z_count + kBtZB - 1) / kBtZB;
   auto picks = [](int n) {
@@ -269,17 +273,35 @@ static void footprint_box(const BpParams &p, const ConeVoxView *hv, int &bw, int
   bh = hmax + 2;
 }
 
+template <int ZB, int NST>
+static int launch_bp_tma_t(const BpParams &p, const CUtensorMap &map, bool weighted, int bw, int bh,
+                           int stage_floats, cudaStream_t st) {
+  const size_t smem = sizeof(float) * (size_t)stage_floats * NST + 128;
+  auto kern = weighted ? cone_bp_tma_kernel<true, ZB, NST> : cone_bp_tma_kernel<false, ZB, NST>;
+  TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + ZB - 1) / ZB);
+  kern<<<grid, kBtThreads, smem, st>>>(map, p, bw, bh, stage_floats);
+  TK_LAUNCHED("cone_bp_tma_kernel");
+  return TK_OK;
+}
+
 int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighted, cudaStream_t st) {
   auto enc = encode_fn();
   if (!enc) return -1;
   if (p.cols % 4 != 0 || (reinterpret_cast<uintptr_t>(p.sino) & 15) != 0) return -1;
   if (p.view_stride != (long long)p.band_rows * p.cols) return -1;
+  const char *ze = getenv("TK_BP_ZB");  // z-voxels per thread: 32 (default) or 16
+  const int zb = ze && atoi(ze) == 16 ? 16 : 32;
   int bw = 0, bh = 0;
-  footprint_box(p, host_views, bw, bh);
+  footprint_box(p, host_views, zb, bw, bh);
   if (bw > 256 || bh > 256) return -1;
   const int stage_floats = ((bw * bh + 31) / 32) * 32;  // 128-byte aligned stages
-  const size_t smem = sizeof(float) * (size_t)stage_floats * kBtStages + 128;
-  if (smem > 200 * 1024) return -1;
+  // stages: as many as fit (<= 8) with two CTAs per SM
+  int nst = kBtMaxStages;
+  while (nst > 2 && sizeof(float) * (size_t)stage_floats * nst + 128 > 110 * 1024) --nst;
+  if (sizeof(float) * (size_t)stage_floats * nst + 128 > 110 * 1024) return -1;
+  nst = nst >= 8 ? 8 : nst >= 6 ? 6 : 4;
+  if (nst == 4 && sizeof(float) * (size_t)stage_floats * 4 + 128 > 110 * 1024) return -1;
 
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)p.cols, (cuuint64_t)p.band_rows, (cuuint64_t)p.n_views};
@@ -290,12 +312,14 @@ int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighte
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -1;
-  auto kern = weighted ? cone_bp_tma_kernel<true> : cone_bp_tma_kernel<false>;
-  TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + kBtZB - 1) / kBtZB);
-  kern<<<grid, kBtThreads, smem, st>>>(map, p, bw, bh, stage_floats);
-  TK_LAUNCHED("cone_bp_tma_kernel");
-  return TK_OK;
+  if (zb == 16) {
+    if (nst == 8) return launch_bp_tma_t<16, 8>(p, map, weighted, bw, bh, stage_floats, st);
+    if (nst == 6) return launch_bp_tma_t<16, 6>(p, map, weighted, bw, bh, stage_floats, st);
+    return launch_bp_tma_t<16, 4>(p, map, weighted, bw, bh, stage_floats, st);
+  }
+  if (nst == 8) return launch_bp_tma_t<32, 8>(p, map, weighted, bw, bh, stage_floats, st);
+  if (nst == 6) return launch_bp_tma_t<32, 6>(p, map, weighted, bw, bh, stage_floats, st);
+  return launch_bp_tma_t<32, 4>(p, map, weighted, bw, bh, stage_floats, st);
 }
 
 }  // namespace tk
