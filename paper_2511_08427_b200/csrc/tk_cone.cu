@@ -295,6 +295,36 @@ __global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny
   }
 }
 
+// Same quads for the y-fastest copy (swap_xy = 1), tiled through shared memory:
+// a 32 (a = y) x 32 (b = x) tile of cells needs a 33 x 33 tap patch that is read
+// along x (coalesced) and written along a (coalesced); the plain kernel reads
+// the transposed orientation with a stride of nx floats (1.97 ms at 512^3).
+__global__ void __launch_bounds__(256) quad_volume_swap_kernel(const float *__restrict__ vol, int nz, int ny,
+                                                               int nx, float4 *__restrict__ q, int diff) {
+  __shared__ float tile[33][34];  // [a - a0][b - b0]
+  constexpr int m = kFpMargin;
+  const int pa = ny + 2 * m, pb = nx + 2 * m;
+  const int a0 = blockIdx.x * 32 - m, b0 = blockIdx.y * 32 - m, z = (int)blockIdx.z - m;
+  const bool zin = (unsigned)z < (unsigned)nz;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int da = e / 33, db = e % 33;  // consecutive threads: consecutive b = x
+    const int y = a0 + da, x = b0 + db;
+    float val = 0.f;
+    if (zin && (unsigned)y < (unsigned)ny && (unsigned)x < (unsigned)nx)
+      val = __ldg(vol + ((long long)z * ny + y) * nx + x);
+    tile[da][db] = val;
+  }
+  __syncthreads();
+  const int ta = threadIdx.x & 31;
+  for (int tb = threadIdx.x >> 5; tb < 32; tb += 8) {
+    const int a = a0 + ta, b = b0 + tb;  // cell (z, b, a) of the y-fastest copy
+    if (a + m >= pa || b + m >= pb) continue;
+    const float v0 = tile[ta][tb], v1 = tile[ta + 1][tb], v2 = tile[ta][tb + 1], v3 = tile[ta + 1][tb + 1];
+    q[((long long)(z + m) * pb + (b + m)) * pa + (a + m)] =
+        diff ? make_float4(v0, v1 - v0, v2, v3 - v2) : make_float4(v0, v1, v2, v3);
+  }
+}
+
 // WR = detector rows per warp: lane l takes row l % WR, column l / WR, so a
 // quarter-warp (8 lanes) spans min(WR, 8) rows of one to eight columns.  Rays of
 // one column march through the same (a, b) cells in near lock-step (they
@@ -1670,9 +1700,14 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       plane_quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst));
       TK_LAUNCHED("plane_quad_volume_kernel");
     } else {
-      quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst),
-                                                plan->diff ? 1 : 0);
-      TK_LAUNCHED("quad_volume_kernel");
+      if (sw) {
+        dim3 tg(ceil_div(ny + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), nz + 2 * kFpMargin);
+        quad_volume_swap_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(dst), plan->diff ? 1 : 0);
+        TK_LAUNCHED("quad_volume_swap_kernel");
+      } else {
+        quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, static_cast<float4 *>(dst), plan->diff ? 1 : 0);
+        TK_LAUNCHED("quad_volume_kernel");
+      }
     }
   }
   return TK_OK;
