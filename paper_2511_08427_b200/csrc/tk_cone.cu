@@ -265,50 +265,29 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
 // so a cell is 2 LDG.128 (slices z and z+1) instead of 8 LDG.32.
 // Same traversal, ordering, arithmetic order of weights as cone_fp2_kernel.
 // ---------------------------------------------------------------------------
-// diff = 1 stores (v00, v01 - v00, v10, v11 - v10) (fast-axis differences
-// pre-subtracted: the sample's fast-axis lerps become single FFMAs with the same
-// fp32 rounding as fmaf(w, b - a, a), i.e. bit-identical results).
-__global__ void quad_volume_kernel(const float *__restrict__ vol, int nz, int ny, int nx, int swap_xy,
-                                   float4 *__restrict__ q, int diff = 0) {
-  constexpr int m = kFpMargin;
-  const int na = swap_xy ? ny : nx, nb = swap_xy ? nx : ny;
-  const int pa = na + 2 * m, pb = nb + 2 * m, pz = nz + 2 * m;
-  const long long total = (long long)pz * pb * pa;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int a = (int)(i % pa) - m;
-    const long long t = i / pa;
-    const int b = (int)(t % pb) - m;
-    const int z = (int)(t / pb) - m;
-    float v[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int aa = a + (j & 1), bb = b + (j >> 1);
-      float val = 0.f;
-      if ((unsigned)z < (unsigned)nz && (unsigned)aa < (unsigned)na && (unsigned)bb < (unsigned)nb) {
-        const int x = swap_xy ? bb : aa, y = swap_xy ? aa : bb;
-        val = __ldg(vol + ((long long)z * ny + y) * nx + x);
-      }
-      v[j] = val;
-    }
-    q[i] = diff ? make_float4(v[0], v[1] - v[0], v[2], v[3] - v[2]) : make_float4(v[0], v[1], v[2], v[3]);
-  }
-}
-
-// Same quads for the y-fastest copy (swap_xy = 1), tiled through shared memory:
-// a 32 (a = y) x 32 (b = x) tile of cells needs a 33 x 33 tap patch that is read
-// along x (coalesced) and written along a (coalesced); the plain kernel reads
-// the transposed orientation with a stride of nx floats (1.97 ms at 512^3).
-__global__ void __launch_bounds__(256) quad_volume_swap_kernel(const float *__restrict__ vol, int nz, int ny,
-                                                               int nx, float4 *__restrict__ q, int diff) {
+// Tap quads of the orientation copies: every margin-padded cell (z, b, a) stores
+// Q[z][b][a] = (V[z][b][a], V[z][b][a+1], V[z][b+1][a], V[z][b+1][a+1]); diff = 1
+// stores (v00, v01 - v00, v10, v11 - v10) (fast-axis differences pre-subtracted:
+// the sample's fast-axis lerps become single FFMAs with the same fp32 rounding as
+// fmaf(w, b - a, a), i.e. bit-identical results).
+// Built tiled through shared memory: a 32 (a) x 32 (b) tile of cells needs a
+// 33 x 33 tap patch, read along x (coalesced) and written along a (coalesced);
+// a per-cell gather reads the y-fastest copy (SWAP) with a stride of nx floats
+// (1.97 ms at 512^3 -> 0.60 ms tiled).
+template <bool SWAP>
+__global__ void __launch_bounds__(256) quad_volume_tiled_kernel(const float *__restrict__ vol, int nz, int ny,
+                                                                int nx, float4 *__restrict__ q, int diff) {
   __shared__ float tile[33][34];  // [a - a0][b - b0]
   constexpr int m = kFpMargin;
-  const int pa = ny + 2 * m, pb = nx + 2 * m;
+  const int na = SWAP ? ny : nx, nb = SWAP ? nx : ny;
+  const int pa = na + 2 * m, pb = nb + 2 * m;
   const int a0 = blockIdx.x * 32 - m, b0 = blockIdx.y * 32 - m, z = (int)blockIdx.z - m;
   const bool zin = (unsigned)z < (unsigned)nz;
   for (int e = threadIdx.x; e < 33 * 33; e += 256) {
-    const int da = e / 33, db = e % 33;  // consecutive threads: consecutive b = x
-    const int y = a0 + da, x = b0 + db;
+    // consecutive threads read consecutive x: x = b for SWAP, x = a otherwise
+    const int da = SWAP ? e / 33 : e % 33, db = SWAP ? e % 33 : e / 33;
+    const int a = a0 + da, b = b0 + db;
+    const int x = SWAP ? b : a, y = SWAP ? a : b;
     float val = 0.f;
     if (zin && (unsigned)y < (unsigned)ny && (unsigned)x < (unsigned)nx)
       val = __ldg(vol + ((long long)z * ny + y) * nx + x);
@@ -317,7 +296,7 @@ __global__ void __launch_bounds__(256) quad_volume_swap_kernel(const float *__re
   __syncthreads();
   const int ta = threadIdx.x & 31;
   for (int tb = threadIdx.x >> 5; tb < 32; tb += 8) {
-    const int a = a0 + ta, b = b0 + tb;  // cell (z, b, a) of the y-fastest copy
+    const int a = a0 + ta, b = b0 + tb;  // cell (z, b, a) of the copy
     if (a + m >= pa || b + m >= pb) continue;
     const float v0 = tile[ta][tb], v1 = tile[ta + 1][tb], v2 = tile[ta][tb + 1], v3 = tile[ta + 1][tb + 1];
     q[((long long)(z + m) * pb + (b + m)) * pa + (a + m)] =
@@ -389,7 +368,7 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
       hi4 = __ldg(p + ps);
     }
     const float wa = fa - la, wb = fb - lb;
-    if (MAGIC) {  // difference quads (quad_volume_kernel diff = 1)
+    if (MAGIC) {  // difference quads (quad_volume_tiled_kernel diff = 1)
       const float s0 = lerpf(fmaf(wa, lo4.y, lo4.x), fmaf(wa, lo4.w, lo4.z), wb);
       const float s1 = lerpf(fmaf(wa, hi4.y, hi4.x), fmaf(wa, hi4.w, hi4.z), wb);
       return lerpf(s0, s1, fz - lz);
@@ -1700,14 +1679,13 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       plane_quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, sw, static_cast<float4 *>(dst));
       TK_LAUNCHED("plane_quad_volume_kernel");
     } else {
-      if (sw) {
-        dim3 tg(ceil_div(ny + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), nz + 2 * kFpMargin);
-        quad_volume_swap_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(dst), plan->diff ? 1 : 0);
-        TK_LAUNCHED("quad_volume_swap_kernel");
-      } else {
-        quad_volume_kernel<<<qgrid, 256, 0, st>>>(vol, nz, ny, nx, 0, static_cast<float4 *>(dst), plan->diff ? 1 : 0);
-        TK_LAUNCHED("quad_volume_kernel");
-      }
+      const int na = sw ? ny : nx, nb = sw ? nx : ny;
+      dim3 tg(ceil_div(na + 2 * kFpMargin, 32), ceil_div(nb + 2 * kFpMargin, 32), nz + 2 * kFpMargin);
+      if (sw)
+        quad_volume_tiled_kernel<true><<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(dst), plan->diff);
+      else
+        quad_volume_tiled_kernel<false><<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(dst), plan->diff);
+      TK_LAUNCHED("quad_volume_tiled_kernel");
     }
   }
   return TK_OK;
