@@ -331,12 +331,20 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     *dst = 0.f;
     return;
   }
-  const float4 *q = W.swap ? qB : qA;
-  const int na = W.swap ? ny : nx, nb = W.swap ? nx : ny;
-  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
-  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  // Orientation copy per ray (W.face_copy) or per view.  At march step k the
+  // sample points of neighbouring rays lie on a plane parallel to the box face
+  // the rays entered through (same t - t0), so a ray that entered through an
+  // x face has its neighbours spread along y: the y-fastest copy keeps a
+  // quarter-warp's taps in one or two 128-byte lines, the x-fastest copy would
+  // put every lane in a different line.  Rays entering through a z face spread
+  // along the detector u direction (the per-view choice).
+  const int swap = W.face_copy ? (rs.face == 0 ? 1 : (rs.face == 1 ? 0 : W.swap)) : W.swap;
+  const float4 *q = swap ? qB : qA;
+  const int na = swap ? ny : nx, nb = swap ? nx : ny;
+  const float ea = (swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (swap ? rs.ex : rs.ey) + (kFpMargin - 1);
   const float ez = rs.ez + (kFpMargin - 1);
-  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const float ga = swap ? rs.gy : rs.gx, gb = swap ? rs.gx : rs.gy, gz = rs.gz;
   const int pa = na + 2 * kFpMargin;
   const int ps = (nb + 2 * kFpMargin) * pa;
   const float paf = (float)pa;
@@ -1700,13 +1708,15 @@ static void fp_plan_free(FpPlan *plan, cudaStream_t st) {
 static int fp_plan_project(const FpPlan &pl, const double *sources, const double *minv, int n_views,
                            int rows, int cols, double step, float *out, cudaStream_t st) {
   std::vector<Fp2View> hv(n_views);
+  const char *fce = getenv("TK_FP_FACE");  // 1 (default): orientation copy per ray from its entry face
+  const int face_copy = fce ? atoi(fce) : 1;
   for (int i = 0; i < n_views; ++i) {
     for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
     for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
     // detector u direction (column 0 of M^-1) in voxel units picks the copy
     const double ux = fabs(minv[9 * i + 0] / pl.sx), uy = fabs(minv[9 * i + 3] / pl.sy);
     hv[i].swap = uy > ux ? 1 : 0;
-    hv[i].pad = 0;
+    hv[i].face_copy = face_copy;
   }
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
@@ -1766,7 +1776,7 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
     // detector u direction (column 0 of M^-1) in voxel units
     const double ux = fabs(minv[9 * i + 0] / sx), uy = fabs(minv[9 * i + 3] / sy);
     hv[i].swap = uy > ux ? 1 : 0;
-    hv[i].pad = 0;
+    hv[i].face_copy = 0;
     (hv[i].swap ? need_b : need_a) = true;
   }
   Scratch dviews, volA, volB;

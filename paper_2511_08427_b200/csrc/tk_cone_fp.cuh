@@ -16,8 +16,8 @@ constexpr int kFpMargin = 2;
 
 struct Fp2View {
   ConeRayView ray;
-  int swap;  // 1: use the y-fastest copy (x and y exchanged)
-  int pad;
+  int swap;       // 1: use the y-fastest copy (x and y exchanged)
+  int face_copy;  // 1: pick the copy per ray from its entry face (cone_fp4_kernel)
 };
 
 
@@ -30,13 +30,16 @@ struct RaySetup {
   float gx, gy, gz;  // padded-index increment per full step
   int n;             // number of samples (reference loop count)
   float last;        // fraction of a step covered by the last sample (0,1]
+  int face;          // axis (0 x, 1 y, 2 z) whose slab sets the entry t0
 };
 
 __device__ __forceinline__ bool clip_axis(double p, double d, double h, double &t0,
-                                          double &t1) {
+                                          double &t1, int axis, int &face) {
   if (fabs(d) > kTiny) {
     double ta = (-h - p) / d, tb = (h - p) / d;
-    t0 = fmax(t0, fmin(ta, tb));
+    const double tn = fmin(ta, tb);
+    if (tn > t0) face = axis;
+    t0 = fmax(t0, tn);
     t1 = fmin(t1, fmax(ta, tb));
     return true;
   }
@@ -57,9 +60,10 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
   const double px = V.src[0], py = V.src[1], pz = V.src[2];
   // _kernels.py:125-130 (_clip_ray_3d on the half-extents (n+1) s / 2)
   double t0 = -1e300, t1 = 1e300;
-  if (!clip_axis(px, dx, (nx + 1) * sx / 2.0, t0, t1)) return false;
-  if (!clip_axis(py, dy, (ny + 1) * sy / 2.0, t0, t1)) return false;
-  if (!clip_axis(pz, dz, (nz + 1) * sz / 2.0, t0, t1)) return false;
+  int face = 2;
+  if (!clip_axis(px, dx, (nx + 1) * sx / 2.0, t0, t1, 0, face)) return false;
+  if (!clip_axis(py, dy, (ny + 1) * sy / 2.0, t0, t1, 1, face)) return false;
+  if (!clip_axis(pz, dz, (nz + 1) * sz / 2.0, t0, t1, 2, face)) return false;
   if (!(t0 < t1)) return false;
   // _kernels.py:133: while t < t1 - TINY  ->  n = ceil((t1 - TINY - t0) / step)
   double span = (t1 - kTiny - t0) / step;
@@ -77,6 +81,7 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
   rs.gz = (float)(step * dz / sz);
   rs.n = n;
   rs.last = (float)last;
+  rs.face = face;
   return true;
 }
 
