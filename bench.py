@@ -290,10 +290,19 @@ def run_ours(args):
     from paper_2511_08427_b200.projectors import bp_cone_tensor_ex, fp_tensor
 
     world, rank, local = dist_env()
+    # TK_BENCH_BACKEND=gloo runs the multi-rank code path with several ranks
+    # sharing the visible GPU(s) -- a functional check of the sharding, row bands
+    # and collectives on a 1-GPU box, not a measurement (the driver uses NCCL)
+    backend = os.environ.get("TK_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
 
     geom = tk.circular_cone_geometry(VOL, SPACING, DET, DET_SP, VIEWS, 2 * math.pi, SDD, SID)
