@@ -456,12 +456,13 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
     *dst = 0.f;
     return;
   }
-  const float4 *q = W.swap ? qB : qA;
-  const int na = W.swap ? ny : nx;
-  const float ea = (W.swap ? rs.ey : rs.ex) + (kFpMargin - 1);
-  const float eb = (W.swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const int swap = W.face_copy ? (rs.face == 0 ? 1 : (rs.face == 1 ? 0 : W.swap)) : W.swap;
+  const float4 *q = swap ? qB : qA;
+  const int na = swap ? ny : nx;
+  const float ea = (swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (swap ? rs.ex : rs.ey) + (kFpMargin - 1);
   const float ez = rs.ez + (kFpMargin - 1);
-  const float ga = W.swap ? rs.gy : rs.gx, gb = W.swap ? rs.gx : rs.gy, gz = rs.gz;
+  const float ga = swap ? rs.gy : rs.gx, gb = swap ? rs.gx : rs.gy, gz = rs.gz;
   const unsigned pa = (unsigned)(na + 2 * kFpMargin);
   const unsigned pp = (unsigned)(nz + 2 * kFpMargin) * pa;  // b-plane stride
   const unsigned bias = kFloorBits * (1u + pa + pp);
@@ -845,6 +846,135 @@ __global__ void __launch_bounds__(kFpBX *kFpBY)
   const float kf = (float)nfull + 0.5f * rs.last;
   trilinear_scatter(adjp, nxp, nyp, nzp, fmaf(kf, rs.gx, rs.ex), fmaf(kf, rs.gy, rs.ey),
                     fmaf(kf, rs.gz, rs.ez), g * rs.last);
+}
+
+// ---------------------------------------------------------------------------
+// Matched adjoint A^T of the forward projector, quad-scatter form ("red4",
+// default).  The exact transpose of cone_fp4_kernel's march: the same rays,
+// CTA order, per-ray orientation copy and sample positions, but each sample
+// SCATTERS y * seg * (trilinear weights) into tap quads of the copy,
+//   Q[z][b][a] += (w(b,a), w(b,a+1), w(b+1,a), w(b+1,a+1)) of slice z,
+// accumulated in registers while the ray stays in one cell and flushed as two
+// vector reductions (REDG.ADD.F32x4: slices z and z+1) when it leaves -- one
+// L2 atomic op per 4 taps instead of 4, and ~1.7 samples per flush.
+// unquad_tiled_kernel then folds the four quads that hold each voxel's tap
+// back into the (z, y, x) volume (the transpose of quad_volume_tiled_kernel).
+// fp32 atomics: the summation order is not deterministic (tolerance 1e-4 vs
+// the oracle's exact transpose, tests/test_gpu_parity.py).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add_v4(float4 *p, const float4 &v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
+    cone_fp_adjoint4_kernel(const float *__restrict__ sino, float4 *__restrict__ qA, float4 *__restrict__ qB,
+                            int nx, int ny, int nz, double sx, double sy, double sz,
+                            const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step) {
+  const int ncb = (cols + kFp2BX - 1) / kFp2BX;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int c = cb * kFp2BX + threadIdx.x;
+  const int r = rb * kFp2BY + threadIdx.y;
+  if (c >= cols || r >= rows) return;
+  const float y = __ldg(sino + ((long long)v * rows + r) * cols + c);
+  if (y == 0.f) return;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
+  const int swap = W.face_copy ? (rs.face == 0 ? 1 : (rs.face == 1 ? 0 : W.swap)) : W.swap;
+  float4 *q = swap ? qB : qA;
+  const int na = swap ? ny : nx, nb = swap ? nx : ny;
+  const float ea = (swap ? rs.ey : rs.ex) + (kFpMargin - 1);
+  const float eb = (swap ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = swap ? rs.gy : rs.gx, gb = swap ? rs.gx : rs.gy, gz = rs.gz;
+  const int pa = na + 2 * kFpMargin;
+  const int ps = (nb + 2 * kFpMargin) * pa;
+  const unsigned bias = kFloorBits * (1u + (unsigned)pa + (unsigned)ps);
+  const float g = y * (float)step;
+  float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+  unsigned cell = 0u;
+  bool open = false;
+  auto sample = [&](float kk, float gs) {
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xz) * (unsigned)ps + (__float_as_uint(xb) * (unsigned)pa + __float_as_uint(xa));
+    if (id != cell) {
+      if (open) {
+        float4 *p = q + (cell - bias);
+        red_add_v4(p, lo);
+        red_add_v4(p + ps, hi);
+      }
+      open = true;
+      cell = id;
+      lo = make_float4(0.f, 0.f, 0.f, 0.f);
+      hi = lo;
+    }
+    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float g1 = gs * wz, g0 = gs - g1;
+    const float l1 = g0 * wb, l0 = g0 - l1, h1 = g1 * wb, h0 = g1 - h1;
+    const float l0a = l0 * wa, l1a = l1 * wa, h0a = h0 * wa, h1a = h1 * wa;
+    lo.x += l0 - l0a;
+    lo.y += l0a;
+    lo.z += l1 - l1a;
+    lo.w += l1a;
+    hi.x += h0 - h0a;
+    hi.y += h0a;
+    hi.z += h1 - h1a;
+    hi.w += h1a;
+  };
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k, kf += 1.f) sample(kf, g);
+  sample((float)nfull + 0.5f * rs.last, g * rs.last);
+  float4 *p = q + (cell - bias);
+  red_add_v4(p, lo);
+  red_add_v4(p + ps, hi);
+}
+
+// vol (+)= fold of one orientation copy's scatter quads: the tap at margin-
+// padded (z, b, a) is Q[b][a].x + Q[b][a-1].y + Q[b-1][a].z + Q[b-1][a-1].w of
+// slice z.  32 (a) x 32 (b) tiles through shared memory so that both the quad
+// reads (along a) and the volume writes (along x) are coalesced for either copy.
+template <bool SWAP>
+__global__ void __launch_bounds__(256) unquad_tiled_kernel(const float4 *__restrict__ q, int nz, int ny, int nx,
+                                                           float *__restrict__ vol, int accumulate) {
+  __shared__ float4 tq[33][33];  // [b - b0 + 1][a - a0 + 1]
+  __shared__ float res[32][33];  // [a - a0][b - b0]
+  constexpr int m = kFpMargin;
+  const int na = SWAP ? ny : nx, nb = SWAP ? nx : ny;
+  const int pa = na + 2 * m, pb = nb + 2 * m;
+  const int a0 = blockIdx.x * 32, b0 = blockIdx.y * 32, z = blockIdx.z;  // real voxel coordinates
+  const long long slice = (long long)(z + m) * pb * pa;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int da = e % 33, db = e / 33;
+    const int pa_i = a0 + m - 1 + da, pb_i = b0 + m - 1 + db;  // padded cell coordinates
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (pa_i < pa && pb_i < pb) val = q[slice + (long long)pb_i * pa + pa_i];
+    tq[db][da] = val;
+  }
+  __syncthreads();
+  const int ta = threadIdx.x & 31;
+  for (int tb = threadIdx.x >> 5; tb < 32; tb += 8)
+    res[ta][tb] = tq[tb + 1][ta + 1].x + tq[tb + 1][ta].y + tq[tb][ta + 1].z + tq[tb][ta].w;
+  __syncthreads();
+  // write along x: x = a (copy A) or x = b (copy B)
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int dx = e & 31, dy = e >> 5;
+    const int da = SWAP ? dy : dx, db = SWAP ? dx : dy;
+    const int a = a0 + da, bb = b0 + db;
+    if (a >= na || bb >= nb) continue;
+    const int x = SWAP ? bb : a, yy = SWAP ? a : bb;
+    float *o = vol + ((long long)z * ny + yy) * nx + x;
+    const float t = res[da][db];
+    *o = accumulate ? *o + t : t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1705,8 +1835,9 @@ static void fp_plan_free(FpPlan *plan, cudaStream_t st) {
   plan->qA = plan->qB = nullptr;
 }
 
-static int fp_plan_project(const FpPlan &pl, const double *sources, const double *minv, int n_views,
-                           int rows, int cols, double step, float *out, cudaStream_t st) {
+// Per-view constants of the orientation-copy kernels (forward and its transpose).
+static std::vector<Fp2View> fp2_views(const double *sources, const double *minv, int n_views, double sx,
+                                      double sy) {
   std::vector<Fp2View> hv(n_views);
   const char *fce = getenv("TK_FP_FACE");  // 1 (default): orientation copy per ray from its entry face
   const int face_copy = fce ? atoi(fce) : 1;
@@ -1714,10 +1845,16 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     for (int j = 0; j < 3; ++j) hv[i].ray.src[j] = sources[3 * i + j];
     for (int j = 0; j < 9; ++j) hv[i].ray.minv[j] = minv[9 * i + j];
     // detector u direction (column 0 of M^-1) in voxel units picks the copy
-    const double ux = fabs(minv[9 * i + 0] / pl.sx), uy = fabs(minv[9 * i + 3] / pl.sy);
+    const double ux = fabs(minv[9 * i + 0] / sx), uy = fabs(minv[9 * i + 3] / sy);
     hv[i].swap = uy > ux ? 1 : 0;
     hv[i].face_copy = face_copy;
   }
+  return hv;
+}
+
+static int fp_plan_project(const FpPlan &pl, const double *sources, const double *minv, int n_views,
+                           int rows, int cols, double step, float *out, cudaStream_t st) {
+  const std::vector<Fp2View> hv = fp2_views(sources, minv, n_views, pl.sx, pl.sy);
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
   dim3 block(kFp2BX, kFp2BY);
@@ -1812,10 +1949,42 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
   return TK_OK;
 }
 
+// A^T y by quad scatter (cone_fp_adjoint4_kernel) + fold (unquad_tiled_kernel).
+static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
+                              const double *sources, const double *minv, int n_views, int rows, int cols,
+                              double step, float *vol, cudaStream_t st) {
+  const std::vector<Fp2View> hv = fp2_views(sources, minv, n_views, sx, sy);
+  Scratch dviews, qA, qB;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
+  constexpr int m2 = 2 * kFpMargin;
+  const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
+  TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
+  const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
+  if (nblocks >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  cone_fp_adjoint4_kernel<8><<<(unsigned)nblocks, dim3(kFp2BX, kFp2BY), 0, st>>>(
+      sino, qA.as<float4>(), qB.as<float4>(), nx, ny, nz, sx, sy, sz, dviews.as<Fp2View>(), rows, cols, n_views,
+      step);
+  TK_LAUNCHED("cone_fp_adjoint4_kernel");
+  unquad_tiled_kernel<false><<<dim3(ceil_div(nx, 32), ceil_div(ny, 32), nz), 256, 0, st>>>(qA.as<float4>(), nz, ny,
+                                                                                          nx, vol, 0);
+  TK_LAUNCHED("unquad_tiled_kernel");
+  unquad_tiled_kernel<true><<<dim3(ceil_div(ny, 32), ceil_div(nx, 32), nz), 256, 0, st>>>(qB.as<float4>(), nz, ny,
+                                                                                         nx, vol, 1);
+  TK_LAUNCHED("unquad_tiled_kernel");
+  return TK_OK;
+}
+
 static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double sy,
                      double sx, const double *sources, const double *minv, int n_views,
                      int rows, int cols, double step, float *out, cudaStream_t st,
                      bool adjoint) {
+  const char *ta = getenv("TK_FPT_ALGO");  // transpose: red4 (default, quad scatter) | scatter (scalar atomics)
+  if (adjoint && !(ta && !strcmp(ta, "scatter")))
+    return launch_fp_adjoint4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   std::vector<ConeRayView> hv(n_views);
   for (int i = 0; i < n_views; ++i) {
     for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];

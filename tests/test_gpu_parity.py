@@ -123,11 +123,12 @@ class TestOracle:
         assert rel(got_fp, sino) < TOL
 
     def test_cfg4_view_subset(self, tk, oracle):
-        """Headline geometry (512^3 @0.5 mm, 1024^2 @0.6 mm) on 4 views spread over
-        the 720-view orbit, full detector resolution."""
+        """Headline geometry (512^3 @0.5 mm, 1024^2 @0.6 mm) on 6 views of the 720-view
+        orbit (0, 22.5, 45, 135, 202.5, 315 degrees: axis-aligned and oblique, where
+        rays enter through both x and y faces), full detector resolution."""
         full = tk.circular_cone_geometry((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6), 720, 2 * np.pi,
                                          1200.0, 750.0)
-        mats = full.matrix_array()[::180]
+        mats = full.matrix_array()[[0, 45, 90, 270, 405, 630]]
         geom = tk.GeometryCone3D((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6),
                                  [tk.ProjectionMatrix(m) for m in mats], 1200.0, 750.0)
         x = tk.phantoms.shepp_logan_3d((512,) * 3)
@@ -393,6 +394,33 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     got = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), gh).data
     want = g.forward_cone_3d(x, (0.9, 1.1, 1.0), gh.matrix_array(), (30, 34), 0.45)
     assert rel(got, want) < TOL
+
+
+@pytest.mark.parametrize("face", ["1", "0"])
+def test_fp_orientation_copy_choice(tk, monkeypatch, face):
+    # per-ray (entry face) vs per-view copy choice: same taps and weights, only the
+    # order of the x / y lerps differs between the two copies (fp32 rounding)
+    geom = tk.circular_cone_geometry((40, 44, 36), (1.0, 0.9, 1.1), (48, 52), (1.6, 1.5), 23, 2 * np.pi,
+                                     1200.0, 750.0)
+    x = torch.randn(40, 44, 36, device="cuda")
+    monkeypatch.setenv("TK_FP_FACE", face)
+    got = tk.forward_project(tk.Volume(x, (1.0, 0.9, 1.1)), geom).data
+    monkeypatch.setenv("TK_FP_FACE", "0" if face == "1" else "1")
+    other = tk.forward_project(tk.Volume(x, (1.0, 0.9, 1.1)), geom).data
+    assert rel(got, other.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("algo", ["red4", "scatter"])
+def test_fp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
+    monkeypatch.setenv("TK_FPT_ALGO", algo)
+    shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
+    hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
+    for mats in (hel, tk.circular_trajectory_3d(13, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4))):
+        geom = tk.GeometryCone3D(shape, sp, (30, 34), (1.5, 1.4), mats, 1200.0, 750.0)
+        y = np.random.default_rng(31).standard_normal((len(mats), 30, 34))
+        got = tk.transpose_forward_project(tk.Sinogram(y, (1.5, 1.4)), geom).data
+        want = oracle.forward_cone_3d_T(y, shape, sp, geom.matrix_array(), 0.45)
+        assert rel(got, want) < TOL
 
 
 def _set_bp_algo(monkeypatch, algo):
