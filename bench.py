@@ -124,14 +124,14 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-FP_KERNEL = "cone_fp4_kernel"  # the default forward projector (TK_FP_ALGO=ldg4m: <.., true>)
+FP_KERNEL = "cone_fp4z_kernel"  # the default forward projector (TK_FP_ALGO=ldg4z)
 BP_KERNEL = "cone_bp_tma_kernel"  # the default back projector (TK_BP_ALGO=tma)
 
 
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernel from the newest committed
     ncu capture of the same configuration (profiles/ncu_*.json)."""
-    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), key=lambda q: q.stat().st_mtime, reverse=True):
+    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), reverse=True):  # newest round/letter first
         try:
             d = json.loads(p.read_text())
         except (ValueError, OSError):

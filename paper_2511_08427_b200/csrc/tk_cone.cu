@@ -395,6 +395,105 @@ __global__ void __launch_bounds__(kFp2BX *kFp2BY, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Forward projection, z-fastest quad variant ("ldg4z").
+//
+// A load instruction costs one L1 data-pipe wavefront per 128-byte line per
+// ACTIVE quarter-warp (8 lanes); a quarter whose lanes all stay in their cells
+// costs nothing (loading unconditionally measured 2.2x slower).  With 8
+// adjacent columns of one row per quarter, every lane crosses cell boundaries
+// along the volume axis that follows the detector u direction at its own steps,
+// so nearly every quarter is active at every step.  Here a quarter is 8
+// consecutive ROWS of one column: their rays lie in one vertical plane through
+// the source and share the horizontal track, so their x / y cell crossings
+// coincide and only z crossings (|gz| <= ~0.12 cell per step at cfg4) are per
+// lane.  The taps are stored z-fastest so the quarter's ~6 consecutive z cells
+// are contiguous:  Qz[y][x][z] = (V[z][y][x], V[z][y][x+1] - V[z][y][x],
+// V[z+1][y][x], V[z+1][y][x+1] - V[z+1][y][x])  (margin-padded), a cell is
+// Qz[y][x][z] and Qz[y+1][x][z].  One copy serves every view.
+// ---------------------------------------------------------------------------
+// 32 (z) x 32 (x) tiles of one y row: reads along x, writes along z (coalesced).
+__global__ void __launch_bounds__(256) quad_volume_z_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
+                                                            float4 *__restrict__ q) {
+  __shared__ float tile[33][34];  // [x - x0][z - z0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, px = nx + 2 * m;
+  const int z0 = blockIdx.x * 32 - m, x0 = blockIdx.y * 32 - m, y = (int)blockIdx.z - m;
+  const bool yin = (unsigned)y < (unsigned)ny;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int dx = e % 33, dz = e / 33;
+    const int x = x0 + dx, z = z0 + dz;
+    float val = 0.f;
+    if (yin && (unsigned)z < (unsigned)nz && (unsigned)x < (unsigned)nx)
+      val = __ldg(vol + ((long long)z * ny + y) * nx + x);
+    tile[dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8) {
+    const int z = z0 + tz, x = x0 + tx;  // cell (z, y, x) of the padded grid
+    if (z + m >= pz || x + m >= px) continue;
+    const float v00 = tile[tx][tz], v01 = tile[tx + 1][tz], v10 = tile[tx][tz + 1], v11 = tile[tx + 1][tz + 1];
+    q[((long long)(y + m) * px + (x + m)) * pz + (z + m)] = make_float4(v00, v01 - v00, v10, v11 - v10);
+  }
+}
+
+constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
+                     const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
+                     float *__restrict__ out) {
+  // CTA = 4 warps x (4 columns x 8 rows) = 16 columns x 8 rows; view-major order
+  constexpr int kCols = 16;
+  const int ncb = (cols + kCols - 1) / kCols;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = cb * kCols + warp * 4 + (lane >> 3);
+  const int r = rb * kFpzRows + (lane & 7);
+  if (c >= cols || r >= rows) return;
+  float *dst = out + ((long long)v * rows + r) * cols + c;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
+    *dst = 0.f;
+    return;
+  }
+  const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
+  const float gx = rs.gx, gy = rs.gy, gz = rs.gz;
+  const unsigned pz = (unsigned)(nz + 2 * kFpMargin);
+  const unsigned sxs = pz, sys = (unsigned)(nx + 2 * kFpMargin) * pz;  // x and y strides (cells)
+  const unsigned bias = kFloorBits * (1u + sxs + sys);
+  unsigned cell = 0xffffffffu;
+  float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
+  auto sample = [&](float kk) -> float {
+    const float fx = fmaf(kk, gx, ex), fy = fmaf(kk, gy, ey), fz = fmaf(kk, gz, ez);
+    const float xx = floor_magic(fx), xy = floor_magic(fy), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xy) * sys + (__float_as_uint(xx) * sxs + __float_as_uint(xz));
+    if (id != cell) {
+      cell = id;
+      const float4 *p = elem_ptr(q, id - bias);
+      lo4 = __ldg(p);
+      hi4 = __ldg(p + sys);
+    }
+    const float wx = fx - (xx - kFloorMagic), wy = fy - (xy - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float s0 = lerpf(fmaf(wx, lo4.y, lo4.x), fmaf(wx, lo4.w, lo4.z), wz);
+    const float s1 = lerpf(fmaf(wx, hi4.y, hi4.x), fmaf(wx, hi4.w, hi4.z), wz);
+    return lerpf(s0, s1, wy);
+  };
+  float acc = 0.f;
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+#pragma unroll 2
+  for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+  acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
+  *dst = acc * (float)step;
+}
+
+// ---------------------------------------------------------------------------
 // Forward projection, b-plane quad variant ("ldg4p").
 //
 // Rays travel mostly along the middle axis b (the orientation copy puts the
@@ -974,6 +1073,107 @@ __global__ void __launch_bounds__(256) unquad_tiled_kernel(const float4 *__restr
     float *o = vol + ((long long)z * ny + yy) * nx + x;
     const float t = res[da][db];
     *o = accumulate ? *o + t : t;
+  }
+}
+
+// z-fastest form of the quad scatter (the transpose of cone_fp4z_kernel, "red4z",
+// default): quarter = 8 rows of one column, so lanes flush together into
+// contiguous quads (coalesced vector reductions); one scatter buffer
+// Qz[y][x][z] += (w(z,x), w(z,x+1), w(z+1,x), w(z+1,x+1)) of row y.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, float4 *__restrict__ q, int nx, int ny, int nz,
+                             double sx, double sy, double sz, const Fp2View *__restrict__ views, int rows,
+                             int cols, int n_views, double step) {
+  constexpr int kCols = 16;
+  const int ncb = (cols + kCols - 1) / kCols;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = cb * kCols + warp * 4 + (lane >> 3);
+  const int r = rb * kFpzRows + (lane & 7);
+  if (c >= cols || r >= rows) return;
+  const float y = __ldg(sino + ((long long)v * rows + r) * cols + c);
+  if (y == 0.f) return;
+  const Fp2View W = views[v];
+  RaySetup rs;
+  if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
+  const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
+  const float gx = rs.gx, gy = rs.gy, gz = rs.gz;
+  const unsigned pz = (unsigned)(nz + 2 * kFpMargin);
+  const unsigned sxs = pz, sys = (unsigned)(nx + 2 * kFpMargin) * pz;
+  const unsigned bias = kFloorBits * (1u + sxs + sys);
+  const float g = y * (float)step;
+  float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+  unsigned cell = 0u;
+  bool open = false;
+  auto sample = [&](float kk, float gs) {
+    const float fx = fmaf(kk, gx, ex), fy = fmaf(kk, gy, ey), fz = fmaf(kk, gz, ez);
+    const float xx = floor_magic(fx), xy = floor_magic(fy), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xy) * sys + (__float_as_uint(xx) * sxs + __float_as_uint(xz));
+    if (id != cell) {
+      if (open) {
+        float4 *p = q + (cell - bias);
+        red_add_v4(p, lo);
+        red_add_v4(p + sys, hi);
+      }
+      open = true;
+      cell = id;
+      lo = make_float4(0.f, 0.f, 0.f, 0.f);
+      hi = lo;
+    }
+    const float wx = fx - (xx - kFloorMagic), wy = fy - (xy - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float g1 = gs * wy, g0 = gs - g1;
+    const float l1 = g0 * wz, l0 = g0 - l1, h1 = g1 * wz, h0 = g1 - h1;
+    const float l0a = l0 * wx, l1a = l1 * wx, h0a = h0 * wx, h1a = h1 * wx;
+    lo.x += l0 - l0a;
+    lo.y += l0a;
+    lo.z += l1 - l1a;
+    lo.w += l1a;
+    hi.x += h0 - h0a;
+    hi.y += h0a;
+    hi.z += h1 - h1a;
+    hi.w += h1a;
+  };
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k, kf += 1.f) sample(kf, g);
+  sample((float)nfull + 0.5f * rs.last, g * rs.last);
+  float4 *p = q + (cell - bias);
+  red_add_v4(p, lo);
+  red_add_v4(p + sys, hi);
+}
+
+// vol = fold of the z-fastest scatter quads: the tap at padded (z, y, x) is
+// Qz[y][x][z].x + Qz[y][x-1][z].y + Qz[y][x][z-1].z + Qz[y][x-1][z-1].w.
+// 32 (z) x 32 (x) tiles of one y row: quad reads along z, volume writes along x.
+__global__ void __launch_bounds__(256) unquad_z_kernel(const float4 *__restrict__ q, int nz, int ny, int nx,
+                                                       float *__restrict__ vol) {
+  __shared__ float4 tq[33][33];  // [x - x0 + 1][z - z0 + 1]
+  __shared__ float res[32][33];  // [z - z0][x - x0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, px = nx + 2 * m;
+  const int z0 = blockIdx.x * 32, x0 = blockIdx.y * 32, y = blockIdx.z;  // real voxel coordinates
+  const long long row = (long long)(y + m) * px;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int dz = e % 33, dx = e / 33;
+    const int zi = z0 + m - 1 + dz, xi = x0 + m - 1 + dx;  // padded cell coordinates
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zi < pz && xi < px) val = q[(row + xi) * pz + zi];
+    tq[dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8)
+    res[tz][tx] = tq[tx + 1][tz + 1].x + tq[tx][tz + 1].y + tq[tx + 1][tz].z + tq[tx][tz].w;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int dx = e & 31, dz = e >> 5;
+    const int x = x0 + dx, z = z0 + dz;
+    if (x < nx && z < nz) vol[((long long)z * ny + y) * nx + x] = res[dz][dx];
   }
 }
 
@@ -1763,8 +1963,8 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg4m (default) | ldg4p | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
-enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg4p, kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg4z (default) | ldg4m | ldg4p | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg4z, kLdg4p, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
@@ -1775,7 +1975,8 @@ static FpAlgo fp_algo() {
   if (e && !strcmp(e, "hwtex")) return FpAlgo::kHwTex;
   if (e && !strcmp(e, "ldg8")) return FpAlgo::kLdg8;
   if (e && !strcmp(e, "ldg4p")) return FpAlgo::kLdg4p;
-  return FpAlgo::kLdg4m;
+  if (e && !strcmp(e, "ldg4m")) return FpAlgo::kLdg4m;
+  return FpAlgo::kLdg4z;
 }
 
 // A forward-projection plan: the two orientation copies of one volume (8-
@@ -1788,6 +1989,7 @@ struct FpPlan {
   bool coef = true;   // Cell8 (ldg8) or float4 quads (ldg4 / ldg4m)
   bool diff = false;  // difference quads (ldg4m)
   bool plane = false; // b-plane difference quads (ldg4p)
+  bool zfast = false; // one z-fastest difference-quad copy (ldg4z)
   void *qA = nullptr, *qB = nullptr;
 };
 
@@ -1802,11 +2004,18 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->coef = fp_algo() == FpAlgo::kLdg8;
   plan->diff = fp_algo() == FpAlgo::kLdg4m;
   plan->plane = fp_algo() == FpAlgo::kLdg4p;
+  plan->zfast = fp_algo() == FpAlgo::kLdg4z;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
   const size_t esz = plan->coef ? sizeof(Cell8) : sizeof(float4);
   TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * ncell, st));
+  if (plan->zfast) {
+    dim3 tg(ceil_div(nz + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), ny + 2 * kFpMargin);
+    quad_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
+    TK_LAUNCHED("quad_volume_z_kernel");
+    return TK_OK;
+  }
   TK_TRY_CUDA(cudaMallocAsync(&plan->qB, esz * ncell, st));
   for (int sw = 0; sw < 2; ++sw) {
     void *dst = sw ? plan->qB : plan->qA;
@@ -1872,6 +2081,13 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
+  } else if (pl.zfast) {
+    const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+    if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
+    auto kern = minb >= 12 ? cone_fp4z_kernel<12> : (minb >= 10 ? cone_fp4z_kernel<10> : cone_fp4z_kernel<8>);
+    kern<<<(unsigned)nbz, 128, 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
+                                        pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out);
+    TK_LAUNCHED("cone_fp4z_kernel");
   } else if (pl.plane) {
     auto kern = mb && minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;  // 10: no spills (measured best)
     kern<<<(unsigned)nblocks, block, 0, st>>>(static_cast<const float4 *>(pl.qA), static_cast<const float4 *>(pl.qB),
@@ -1952,7 +2168,7 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
 // A^T y by quad scatter (cone_fp_adjoint4_kernel) + fold (unquad_tiled_kernel).
 static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
                               const double *sources, const double *minv, int n_views, int rows, int cols,
-                              double step, float *vol, cudaStream_t st) {
+                              double step, float *vol, cudaStream_t st, bool zfast) {
   const std::vector<Fp2View> hv = fp2_views(sources, minv, n_views, sx, sy);
   Scratch dviews, qA, qB;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
@@ -1960,6 +2176,18 @@ static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double 
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
   TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
+  if (zfast) {
+    TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
+    const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+    if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+    cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.as<float4>(), nx, ny, nz, sx, sy, sz,
+                                                               dviews.as<Fp2View>(), rows, cols, n_views, step);
+    TK_LAUNCHED("cone_fp_adjoint4z_kernel");
+    unquad_z_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qA.as<float4>(), nz, ny, nx,
+                                                                                 vol);
+    TK_LAUNCHED("unquad_z_kernel");
+    return TK_OK;
+  }
   TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
   TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
@@ -1982,9 +2210,11 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
                      double sx, const double *sources, const double *minv, int n_views,
                      int rows, int cols, double step, float *out, cudaStream_t st,
                      bool adjoint) {
-  const char *ta = getenv("TK_FPT_ALGO");  // transpose: red4 (default, quad scatter) | scatter (scalar atomics)
+  // transpose: red4z (default, z-fastest quad scatter) | red4 (orientation-copy quads) | scatter (scalar atomics)
+  const char *ta = getenv("TK_FPT_ALGO");
   if (adjoint && !(ta && !strcmp(ta, "scatter")))
-    return launch_fp_adjoint4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
+    return launch_fp_adjoint4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st,
+                              !(ta && !strcmp(ta, "red4")));
   std::vector<ConeRayView> hv(n_views);
   for (int i = 0; i < n_views; ++i) {
     for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
@@ -1995,7 +2225,8 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 block(kFpBX, kFpBY);
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
-  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m || algo == FpAlgo::kLdg4p))
+  if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m || algo == FpAlgo::kLdg4p ||
+                   algo == FpAlgo::kLdg4z))
     return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);

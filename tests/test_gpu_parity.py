@@ -378,7 +378,7 @@ class TestProperties:
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("algo", ["ldg4m", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["ldg4m", "ldg4z", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
 def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     monkeypatch.setenv("TK_FP_ALGO", algo)
     geom = tk.GeometryCone3D((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4),
@@ -410,7 +410,7 @@ def test_fp_orientation_copy_choice(tk, monkeypatch, face):
     assert rel(got, other.cpu().numpy()) < 1e-6
 
 
-@pytest.mark.parametrize("algo", ["red4", "scatter"])
+@pytest.mark.parametrize("algo", ["red4z", "red4", "scatter"])
 def test_fp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
     monkeypatch.setenv("TK_FPT_ALGO", algo)
     shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
