@@ -437,8 +437,42 @@ __global__ void __launch_bounds__(256) quad_volume_z_kernel(const float *__restr
   }
 }
 
+// Coefficient form ("ldg4z", default): each cell of row y stores the bilinear
+// (x, z) polynomial of its taps,  Cz[y][x][z] = (A, B, C, D) with A = V00,
+// B = V01 - V00, C = V10 - V00, D = (V11 - V10) - (V01 - V00)  (V_zx of row y),
+// so a row is  P = fma(wz, fma(wx, D, C), fma(wx, B, A))  (3 FFMA instead of 4
+// FFMA + FADD) and a sample is lerp(P(Cz[y]), P(Cz[y+1]), wy).  (A second array
+// of y differences, s = P(C) + wy P(dC), saves one more FADD but loses the L1
+// sharing between a cell's y+1 row and the next cell's y row: measured 776 ms
+// vs 489 ms.)
+__global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
+                                                            float4 *__restrict__ cq) {
+  __shared__ float tile[33][34];  // [x - x0][z - z0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, px = nx + 2 * m;
+  const int z0 = blockIdx.x * 32 - m, x0 = blockIdx.y * 32 - m, y = (int)blockIdx.z - m;
+  const bool yin = (unsigned)y < (unsigned)ny;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int dx = e % 33, dz = e / 33;
+    const int x = x0 + dx, z = z0 + dz;
+    float val = 0.f;
+    if (yin && (unsigned)z < (unsigned)nz && (unsigned)x < (unsigned)nx)
+      val = __ldg(vol + ((long long)z * ny + y) * nx + x);
+    tile[dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8) {
+    const int z = z0 + tz, x = x0 + tx;  // cell (z, y, x) of the padded grid
+    if (z + m >= pz || x + m >= px) continue;
+    const float v00 = tile[tx][tz], v01 = tile[tx + 1][tz], v10 = tile[tx][tz + 1], v11 = tile[tx + 1][tz + 1];
+    cq[((long long)(y + m) * px + (x + m)) * pz + (z + m)] =
+        make_float4(v00, v01 - v00, v10 - v00, (v11 - v10) - (v01 - v00));
+  }
+}
+
 constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
-template <int MINB>
+template <int MINB, bool COEF>
 __global__ void __launch_bounds__(128, MINB)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
@@ -480,6 +514,11 @@ __global__ void __launch_bounds__(128, MINB)
       hi4 = __ldg(p + sys);
     }
     const float wx = fx - (xx - kFloorMagic), wy = fy - (xy - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    if (COEF) {
+      const float s0 = fmaf(wz, fmaf(wx, lo4.w, lo4.z), fmaf(wx, lo4.y, lo4.x));
+      const float s1 = fmaf(wz, fmaf(wx, hi4.w, hi4.z), fmaf(wx, hi4.y, hi4.x));
+      return lerpf(s0, s1, wy);
+    }
     const float s0 = lerpf(fmaf(wx, lo4.y, lo4.x), fmaf(wx, lo4.w, lo4.z), wz);
     const float s1 = lerpf(fmaf(wx, hi4.y, hi4.x), fmaf(wx, hi4.w, hi4.z), wz);
     return lerpf(s0, s1, wy);
@@ -1963,8 +2002,8 @@ static void pack_bp_views(const double *mats, int n_views, double sx, double sy,
   }
 }
 
-// Forward-projector algorithm: TK_FP_ALGO = ldg4z (default) | ldg4m | ldg4p | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
-enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg4z, kLdg4p, kLdg2, kTex, kLdg, kHwTex };
+// Forward-projector algorithm: TK_FP_ALGO = ldg4z (default) | ldg4zq | ldg4m | ldg4p | ldg4 | ldg8 | ldg2 | ldg | tex | hwtex.
+enum class FpAlgo { kLdg8, kLdg4, kLdg4m, kLdg4z, kLdg4zq, kLdg4p, kLdg2, kTex, kLdg, kHwTex };
 
 static FpAlgo fp_algo() {
   const char *e = getenv("TK_FP_ALGO");
@@ -1976,6 +2015,7 @@ static FpAlgo fp_algo() {
   if (e && !strcmp(e, "ldg8")) return FpAlgo::kLdg8;
   if (e && !strcmp(e, "ldg4p")) return FpAlgo::kLdg4p;
   if (e && !strcmp(e, "ldg4m")) return FpAlgo::kLdg4m;
+  if (e && !strcmp(e, "ldg4zq")) return FpAlgo::kLdg4zq;
   return FpAlgo::kLdg4z;
 }
 
@@ -2004,7 +2044,8 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   plan->coef = fp_algo() == FpAlgo::kLdg8;
   plan->diff = fp_algo() == FpAlgo::kLdg4m;
   plan->plane = fp_algo() == FpAlgo::kLdg4p;
-  plan->zfast = fp_algo() == FpAlgo::kLdg4z;
+  plan->zfast = fp_algo() == FpAlgo::kLdg4z || fp_algo() == FpAlgo::kLdg4zq;
+  if (plan->zfast) plan->diff = fp_algo() == FpAlgo::kLdg4zq;
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
@@ -2012,8 +2053,13 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * ncell, st));
   if (plan->zfast) {
     dim3 tg(ceil_div(nz + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), ny + 2 * kFpMargin);
-    quad_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
-    TK_LAUNCHED("quad_volume_z_kernel");
+    if (plan->diff) {  // quads (ldg4zq)
+      quad_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
+      TK_LAUNCHED("quad_volume_z_kernel");
+    } else {  // coefficient cells (ldg4z)
+      coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
+      TK_LAUNCHED("coef_volume_z_kernel");
+    }
     return TK_OK;
   }
   TK_TRY_CUDA(cudaMallocAsync(&plan->qB, esz * ncell, st));
@@ -2084,7 +2130,8 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   } else if (pl.zfast) {
     const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-    auto kern = minb >= 12 ? cone_fp4z_kernel<12> : (minb >= 10 ? cone_fp4z_kernel<10> : cone_fp4z_kernel<8>);
+    auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)
+                        : (minb >= 12 ? cone_fp4z_kernel<12, true> : cone_fp4z_kernel<10, true>);
     kern<<<(unsigned)nbz, 128, 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
                                         pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out);
     TK_LAUNCHED("cone_fp4z_kernel");
@@ -2226,7 +2273,7 @@ static int launch_fp(const float *vol, int nz, int ny, int nx, double sz, double
   dim3 grid(ceil_div(cols, kFpBX), ceil_div(rows, kFpBY), n_views);
   const FpAlgo algo = fp_algo();
   if (!adjoint && (algo == FpAlgo::kLdg8 || algo == FpAlgo::kLdg4 || algo == FpAlgo::kLdg4m || algo == FpAlgo::kLdg4p ||
-                   algo == FpAlgo::kLdg4z))
+                   algo == FpAlgo::kLdg4z || algo == FpAlgo::kLdg4zq))
     return launch_fp4(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   if (!adjoint && algo == FpAlgo::kLdg2)
     return launch_fp2(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);

@@ -378,7 +378,7 @@ class TestProperties:
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("algo", ["ldg4m", "ldg4z", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["ldg4m", "ldg4z", "ldg4zq", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
 def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     monkeypatch.setenv("TK_FP_ALGO", algo)
     geom = tk.GeometryCone3D((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4),
