@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256) quad_volume_z_kernel(const float *__restr
 // sharing between a cell's y+1 row and the next cell's y row: measured 776 ms
 // vs 489 ms.)
 __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
-                                                            float4 *__restrict__ cq) {
+                                                            float4 *__restrict__ cq, int zpitch, int xpitch) {
   __shared__ float tile[33][34];  // [x - x0][z - z0]
   constexpr int m = kFpMargin;
   const int pz = nz + 2 * m, px = nx + 2 * m;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
     const int z = z0 + tz, x = x0 + tx;  // cell (z, y, x) of the padded grid
     if (z + m >= pz || x + m >= px) continue;
     const float v00 = tile[tx][tz], v01 = tile[tx + 1][tz], v10 = tile[tx][tz + 1], v11 = tile[tx + 1][tz + 1];
-    cq[((long long)(y + m) * px + (x + m)) * pz + (z + m)] =
+    cq[((long long)(y + m) * xpitch + (x + m)) * zpitch + (z + m)] =
         make_float4(v00, v01 - v00, v10 - v00, (v11 - v10) - (v01 - v00));
   }
 }
@@ -476,7 +476,7 @@ template <int MINB, bool COEF>
 __global__ void __launch_bounds__(128, MINB)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
-                     float *__restrict__ out) {
+                     float *__restrict__ out, unsigned zpitch, unsigned xpitch) {
   // CTA = 4 warps x (4 columns x 8 rows) = 16 columns x 8 rows; view-major order
   constexpr int kCols = 16;
   const int ncb = (cols + kCols - 1) / kCols;
@@ -498,14 +498,19 @@ __global__ void __launch_bounds__(128, MINB)
   }
   const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
   const float gx = rs.gx, gy = rs.gy, gz = rs.gz;
-  const unsigned pz = (unsigned)(nz + 2 * kFpMargin);
-  const unsigned sxs = pz, sys = (unsigned)(nx + 2 * kFpMargin) * pz;  // x and y strides (cells)
-  const unsigned bias = kFloorBits * (1u + sxs + sys);
+  // COEF layouts use zpitch / xpitch chosen on the host so that the floor bias
+  // 0x4B000000 * (1 + zpitch + xpitch * zpitch) vanishes modulo 2^32: the cell
+  // index formed from the FADD.RM float bits IS the element index (one
+  // IMAD.WIDE per address instead of IADD + LEA + LEA.HI.X).  Coordinates are
+  // >= 0 here, so floor(f) = bits(f + 2^23) - 0x4B000000.
+  const float magic = COEF ? 8388608.f : kFloorMagic;
+  const unsigned sxs = zpitch, sys = xpitch * zpitch;  // x and y strides (cells)
+  const unsigned bias = COEF ? 0u : kFloorBits * (1u + sxs + sys);
   unsigned cell = 0xffffffffu;
   float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
   auto sample = [&](float kk) -> float {
     const float fx = fmaf(kk, gx, ex), fy = fmaf(kk, gy, ey), fz = fmaf(kk, gz, ez);
-    const float xx = floor_magic(fx), xy = floor_magic(fy), xz = floor_magic(fz);
+    const float xx = __fadd_rd(fx, magic), xy = __fadd_rd(fy, magic), xz = __fadd_rd(fz, magic);
     const unsigned id = __float_as_uint(xy) * sys + (__float_as_uint(xx) * sxs + __float_as_uint(xz));
     if (id != cell) {
       cell = id;
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(128, MINB)
       lo4 = __ldg(p);
       hi4 = __ldg(p + sys);
     }
-    const float wx = fx - (xx - kFloorMagic), wy = fy - (xy - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float wx = fx - (xx - magic), wy = fy - (xy - magic), wz = fz - (xz - magic);
     if (COEF) {
       const float s0 = fmaf(wz, fmaf(wx, lo4.w, lo4.z), fmaf(wx, lo4.y, lo4.x));
       const float s1 = fmaf(wz, fmaf(wx, hi4.w, hi4.z), fmaf(wx, hi4.y, hi4.x));
@@ -2029,7 +2034,8 @@ struct FpPlan {
   bool coef = true;   // Cell8 (ldg8) or float4 quads (ldg4 / ldg4m)
   bool diff = false;  // difference quads (ldg4m)
   bool plane = false; // b-plane difference quads (ldg4p)
-  bool zfast = false; // one z-fastest difference-quad copy (ldg4z)
+  bool zfast = false; // one z-fastest copy (ldg4z coefficient cells, ldg4zq difference quads)
+  unsigned zpitch = 0, xpitch = 0;  // z-fastest cell pitches
   void *qA = nullptr, *qB = nullptr;
 };
 
@@ -2050,18 +2056,37 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const unsigned qgrid = (unsigned)std::min<long long>(ceil_div(ncell, 256), (long long)sm_count() * 32);
   const size_t esz = plan->coef ? sizeof(Cell8) : sizeof(float4);
-  TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * ncell, st));
   if (plan->zfast) {
+    plan->zpitch = (unsigned)(nz + m2);
+    plan->xpitch = (unsigned)(nx + m2);
+    if (!plan->diff) {  // bias-free pitches: zp (1 + xp) == -1 (mod 256), zp odd; least padding
+      long long best = -1;
+      for (unsigned zp = (unsigned)(nz + m2) | 1u; zp < (unsigned)(nz + m2) + 128; zp += 2) {
+        unsigned xp = (unsigned)(nx + m2);
+        while ((zp * (1u + xp)) % 256u != 255u) ++xp;
+        const long long cells = (long long)zp * xp;
+        if (best < 0 || cells < best) {
+          best = cells;
+          plan->zpitch = zp;
+          plan->xpitch = xp;
+        }
+      }
+    }
+    const long long nz_cells = (long long)(ny + m2) * plan->xpitch * plan->zpitch;
+    if (nz_cells >= (1LL << 32)) return fail_arg("tk_forward_cone_3d: volume too large for 32-bit cell indices");
+    TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * nz_cells, st));
     dim3 tg(ceil_div(nz + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), ny + 2 * kFpMargin);
     if (plan->diff) {  // quads (ldg4zq)
       quad_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
       TK_LAUNCHED("quad_volume_z_kernel");
     } else {  // coefficient cells (ldg4z)
-      coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
+      coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA), (int)plan->zpitch,
+                                               (int)plan->xpitch);
       TK_LAUNCHED("coef_volume_z_kernel");
     }
     return TK_OK;
   }
+  TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * ncell, st));
   TK_TRY_CUDA(cudaMallocAsync(&plan->qB, esz * ncell, st));
   for (int sw = 0; sw < 2; ++sw) {
     void *dst = sw ? plan->qB : plan->qA;
@@ -2133,7 +2158,8 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)
                         : (minb >= 12 ? cone_fp4z_kernel<12, true> : cone_fp4z_kernel<10, true>);
     kern<<<(unsigned)nbz, 128, 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
-                                        pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out);
+                                        pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out, pl.zpitch,
+                                        pl.xpitch);
     TK_LAUNCHED("cone_fp4z_kernel");
   } else if (pl.plane) {
     auto kern = mb && minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;  // 10: no spills (measured best)
