@@ -11,4 +11,4 @@ timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ec
 cat gpurun_out/bench.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
 cat gpurun_out/bench_ref.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1; echo ncu rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"cone_|coef_|quad|fft_|pad|crop" -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1; echo ncu rc=$?
