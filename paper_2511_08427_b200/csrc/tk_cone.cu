@@ -472,22 +472,24 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
 }
 
 constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
-template <int MINB, bool COEF>
+// RB = detector rows per CTA band (8, 16 or 32): the CTA's 16 quarter-warps
+// cover (128 / RB) columns x RB rows, each quarter 8 consecutive rows of one column.
+template <int MINB, bool COEF, int RB = 8>
 __global__ void __launch_bounds__(128, MINB)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
                      float *__restrict__ out, unsigned zpitch, unsigned xpitch) {
-  // CTA = 4 warps x (4 columns x 8 rows) = 16 columns x 8 rows; view-major order
-  constexpr int kCols = 16;
+  // view-major order within RB-row bands
+  constexpr int kCols = 128 / RB, kQpc = RB / kFpzRows;  // columns per CTA, quarters per column
   const int ncb = (cols + kCols - 1) / kCols;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
   const unsigned bt = b / ncb;
   const int v = (int)(bt % n_views);
   const int rb = (int)(bt / n_views);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = cb * kCols + warp * 4 + (lane >> 3);
-  const int r = rb * kFpzRows + (lane & 7);
+  const int qd = threadIdx.x >> 3;  // quarter-warp index in the CTA
+  const int c = cb * kCols + qd / kQpc;
+  const int r = rb * RB + (qd % kQpc) * kFpzRows + (threadIdx.x & 7);
   if (c >= cols || r >= rows) return;
   float *dst = out + ((long long)v * rows + r) * cols + c;
   const Fp2View W = views[v];
@@ -2153,10 +2155,15 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                               cols, n_views, step, out);
     TK_LAUNCHED("cone_fp8_kernel");
   } else if (pl.zfast) {
-    const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+    const char *rbe = getenv("TK_FPZ_RB");  // detector rows per CTA band: 8 (default), 16, 32
+    const int rbz = rbe ? atoi(rbe) : 8;
+    const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * n_views;
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)
-                        : (minb >= 12 ? cone_fp4z_kernel<12, true> : cone_fp4z_kernel<10, true>);
+                        : (minb >= 12 ? cone_fp4z_kernel<12, true>
+                                      : (minb >= 10 ? cone_fp4z_kernel<10, true> : cone_fp4z_kernel<8, true>));
+    if (!pl.diff && rbz == 16) kern = cone_fp4z_kernel<12, true, 16>;
+    if (!pl.diff && rbz == 32) kern = cone_fp4z_kernel<12, true, 32>;
     kern<<<(unsigned)nbz, 128, 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
                                         pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out, pl.zpitch,
                                         pl.xpitch);
