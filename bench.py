@@ -153,11 +153,19 @@ def gather_roofline(fp_bytes, fp_ms, bp_bytes, bp_ms, clocks):
     if not mhz and p.exists():
         mhz = json.loads(p.read_text()).get("sm_max_mhz")
     mhz = float(mhz or 1965.0)
-    peak = 128.0 * sms * mhz * 1e6 / 1e9  # GB/s
+    per_clk, src = 128.0, "nominal 128 B/clk/SM"
+    probes = sorted((ROOT / "profiles").glob("l1_peak_*.json"), reverse=True)  # scripts/l1_peak.cu
+    if probes:
+        try:
+            per_clk = float(json.loads(probes[0].read_text())["ldg128_bytes_per_clk_sm"])
+            src = f"measured LDG.128 {per_clk:.1f} B/clk/SM (profiles/{probes[0].name}, scripts/l1_peak.cu)"
+        except (ValueError, KeyError, OSError):
+            pass
+    peak = per_clk * sms * mhz * 1e6 / 1e9  # GB/s
     fp = fp_bytes / (fp_ms * 1e-3) / 1e9
     bp = bp_bytes / (bp_ms * 1e-3) / 1e9
     return {"bound": "l1_load_path", "unit": "GB/s", "peak": round(peak, 1),
-            "peak_source": f"128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)",
+            "peak_source": f"{src} x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)",
             "forward": {"kernel": FP_KERNEL, "achieved": round(fp, 1), "frac": round(fp / peak, 4),
                         "bytes_per_unit": "32 B per trilinear sample"},
             "back": {"kernel": BP_KERNEL, "achieved": round(bp, 1), "frac": round(bp / peak, 4),

@@ -1,0 +1,83 @@
+// l1_peak.cu -- measured L1 load-path ceilings on the B200 (the roofline the
+// gather kernels are reported against):
+//   ldg128: every quarter-warp reads one full 128-byte line per LDG.128 from an
+//           L1-resident 32 KB buffer (best case for a vector gather);
+//   lds32:  conflict-free LDS.32, one 128-byte wavefront per warp instruction.
+// Build + run:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/l1_peak scripts/l1_peak.cu && /tmp/l1_peak
+// Prints one JSON line (bytes moved to registers per second, whole GPU).
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int kIters = 4096;
+
+__global__ void __launch_bounds__(256) ldg128_kernel(const float4 *__restrict__ buf, float *out, unsigned mask) {
+  // 2048 float4 = 32 KB per SM-resident working set; lane l of the warp reads
+  // element (base + l): each quarter-warp covers one 128-byte line
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  unsigned idx = (threadIdx.x & ~31u) + (threadIdx.x & 31u);
+#pragma unroll 8
+  for (int i = 0; i < kIters; ++i) {
+    const float4 v = __ldg(buf + (idx & mask));
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+    idx += 256;
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 1234.5f) out[threadIdx.x] = acc.x;
+}
+
+__global__ void __launch_bounds__(256) lds32_kernel(float *out) {
+  __shared__ float sm[8192];
+  for (int i = threadIdx.x; i < 8192; i += 256) sm[i] = (float)i;
+  __syncthreads();
+  float acc = 0.f;
+  unsigned idx = threadIdx.x;
+#pragma unroll 16
+  for (int i = 0; i < kIters; ++i) {
+    acc += sm[idx & 8191u];
+    idx += 32 * 9;  // stays conflict-free: lanes hit 32 consecutive words
+  }
+  if (acc == 1234.5f) out[threadIdx.x] = acc;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);  // kHz (max boost)
+  float4 *buf;
+  float *out;
+  cudaMalloc(&buf, 2048 * sizeof(float4));
+  cudaMemset(buf, 0, 2048 * sizeof(float4));
+  cudaMalloc(&out, 1024 * sizeof(float));
+  const int blocks = sms * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best_ldg = 1e30f, best_lds = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(a);
+    ldg128_kernel<<<blocks, 256>>>(buf, out, 2047u);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep) best_ldg = ms < best_ldg ? ms : best_ldg;
+    cudaEventRecord(a);
+    lds32_kernel<<<blocks, 256>>>(out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep) best_lds = ms < best_lds ? ms : best_lds;
+  }
+  const double ldg_bytes = (double)blocks * 256 * kIters * 16, lds_bytes = (double)blocks * 256 * kIters * 4;
+  const double ldg_gbs = ldg_bytes / (best_ldg * 1e-3) / 1e9, lds_gbs = lds_bytes / (best_lds * 1e-3) / 1e9;
+  const double nominal = 128.0 * sms * clk * 1e3 / 1e9;
+  printf("{\"ldg128_gbs\": %.1f, \"lds32_gbs\": %.1f, \"nominal_128B_per_clk_gbs\": %.1f, \"sms\": %d, "
+         "\"max_clock_mhz\": %.0f, \"ldg128_bytes_per_clk_sm\": %.1f, \"lds32_bytes_per_clk_sm\": %.1f, "
+         "\"err\": \"%s\"}\n",
+         ldg_gbs, lds_gbs, nominal, sms, clk / 1e3, ldg_gbs * 1e9 / (sms * clk * 1e3),
+         lds_gbs * 1e9 / (sms * clk * 1e3), cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

@@ -34,7 +34,10 @@ def test_gather_roofline_fractions():
     import bench
 
     g = bench.gather_roofline(32.0 * 1e12, 1000.0, 16.0 * 1e12, 500.0, {"sm_mhz": 1965.0})
-    peak = 128.0 * 148 * 1965.0 * 1e6 / 1e9
+    # peak = measured LDG.128 bytes/clk/SM (profiles/l1_peak_*.json) x 148 SMs x clock
+    per_clk = json.loads(sorted((ROOT / "profiles").glob("l1_peak_*.json"))[-1].read_text())["ldg128_bytes_per_clk_sm"]
+    peak = per_clk * 148 * 1965.0 * 1e6 / 1e9
+    assert 120.0 <= per_clk <= 128.0 and "measured" in g["peak_source"]
     assert g["peak"] == pytest.approx(peak, abs=0.1)
     assert g["forward"]["achieved"] == pytest.approx(32.0e12 / 1.0 / 1e9, abs=0.1)
     assert g["back"]["frac"] == pytest.approx(16.0e12 / 0.5 / 1e9 / peak, rel=1e-3)
