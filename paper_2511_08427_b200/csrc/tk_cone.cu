@@ -1124,13 +1124,19 @@ __global__ void __launch_bounds__(256) unquad_tiled_kernel(const float4 *__restr
 
 // z-fastest form of the quad scatter (the transpose of cone_fp4z_kernel, "red4z",
 // default): quarter = 8 rows of one column, so lanes flush together into
-// contiguous quads (coalesced vector reductions); one scatter buffer
-// Qz[y][x][z] += (w(z,x), w(z,x+1), w(z+1,x), w(z+1,x+1)) of row y.
+// contiguous quads.  Two scatter buffers, one per horizontal row axis b:
+//   qy: Qz[y][x][z] += (w(z,x), w(z,x+1), w(z+1,x), w(z+1,x+1)) of row y,
+//   qx: Qx[x][y][z] += (w(z,y), w(z,y+1), w(z+1,y), w(z+1,y+1)) of row x;
+// a ray scatters into the buffer whose row axis is its major horizontal axis,
+// so most cell changes are row steps b -> b +- 1, where the new cell's near row
+// is the old cell's far row: that quad's accumulator is carried over in
+// registers and only the row left behind is flushed (one REDG.F32x4 instead of
+// two).
 template <int MINB>
 __global__ void __launch_bounds__(128, MINB)
-    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, float4 *__restrict__ q, int nx, int ny, int nz,
-                             double sx, double sy, double sz, const Fp2View *__restrict__ views, int rows,
-                             int cols, int n_views, double step) {
+    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, float4 *__restrict__ qy, float4 *__restrict__ qx,
+                             int nx, int ny, int nz, double sx, double sy, double sz,
+                             const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step) {
   constexpr int kCols = 16;
   const int ncb = (cols + kCols - 1) / kCols;
   const unsigned b = blockIdx.x;
@@ -1147,34 +1153,48 @@ __global__ void __launch_bounds__(128, MINB)
   const Fp2View W = views[v];
   RaySetup rs;
   if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
-  const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
-  const float gx = rs.gx, gy = rs.gy, gz = rs.gz;
+  const bool xrow = fabsf(rs.gx) > fabsf(rs.gy);  // major horizontal axis (cells per step)
+  float4 *q = xrow ? qx : qy;
+  const float ea = (xrow ? rs.ey : rs.ex) + (kFpMargin - 1), eb = (xrow ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = xrow ? rs.gy : rs.gx, gb = xrow ? rs.gx : rs.gy, gz = rs.gz;
   const unsigned pz = (unsigned)(nz + 2 * kFpMargin);
-  const unsigned sxs = pz, sys = (unsigned)(nx + 2 * kFpMargin) * pz;
-  const unsigned bias = kFloorBits * (1u + sxs + sys);
+  const unsigned sas = pz, sbs = (unsigned)((xrow ? ny : nx) + 2 * kFpMargin) * pz;  // a and b strides
+  const unsigned bias = kFloorBits * (1u + sas + sbs);
   const float g = y * (float)step;
   float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
   unsigned cell = 0u;
   bool open = false;
   auto sample = [&](float kk, float gs) {
-    const float fx = fmaf(kk, gx, ex), fy = fmaf(kk, gy, ey), fz = fmaf(kk, gz, ez);
-    const float xx = floor_magic(fx), xy = floor_magic(fy), xz = floor_magic(fz);
-    const unsigned id = __float_as_uint(xy) * sys + (__float_as_uint(xx) * sxs + __float_as_uint(xz));
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xb) * sbs + (__float_as_uint(xa) * sas + __float_as_uint(xz));
     if (id != cell) {
+      const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
       if (open) {
         float4 *p = q + (cell - bias);
-        red_add_v4(p, lo);
-        red_add_v4(p + sys, hi);
+        const unsigned d = id - cell;
+        if (d == sbs) {  // row b -> b + 1: the far row becomes the near row
+          red_add_v4(p, lo);
+          lo = hi;
+          hi = zero;
+        } else if (d == 0u - sbs) {  // row b -> b - 1: the near row becomes the far row
+          red_add_v4(p + sbs, hi);
+          hi = lo;
+          lo = zero;
+        } else {
+          red_add_v4(p, lo);
+          red_add_v4(p + sbs, hi);
+          lo = hi = zero;
+        }
       }
       open = true;
       cell = id;
-      lo = make_float4(0.f, 0.f, 0.f, 0.f);
-      hi = lo;
     }
-    const float wx = fx - (xx - kFloorMagic), wy = fy - (xy - kFloorMagic), wz = fz - (xz - kFloorMagic);
-    const float g1 = gs * wy, g0 = gs - g1;
+    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float g1 = gs * wb, g0 = gs - g1;
     const float l1 = g0 * wz, l0 = g0 - l1, h1 = g1 * wz, h0 = g1 - h1;
-    const float l0a = l0 * wx, l1a = l1 * wx, h0a = h0 * wx, h1a = h1 * wx;
+    const float l0a = l0 * wa, l1a = l1 * wa, h0a = h0 * wa, h1a = h1 * wa;
     lo.x += l0 - l0a;
     lo.y += l0a;
     lo.z += l1 - l1a;
@@ -1190,7 +1210,37 @@ __global__ void __launch_bounds__(128, MINB)
   sample((float)nfull + 0.5f * rs.last, g * rs.last);
   float4 *p = q + (cell - bias);
   red_add_v4(p, lo);
-  red_add_v4(p + sys, hi);
+  red_add_v4(p + sbs, hi);
+}
+
+// vol += fold of the x-row scatter quads qx: the tap at padded (z, y, x) is
+// Qx[x][y][z].x + Qx[x][y-1][z].y + Qx[x][y][z-1].z + Qx[x][y-1][z-1].w.
+// 32 (z) x 32 (x) tiles of one y: quad reads along z, volume writes along x.
+__global__ void __launch_bounds__(256) unquad_zx_kernel(const float4 *__restrict__ q, int nz, int ny, int nx,
+                                                        float *__restrict__ vol) {
+  __shared__ float4 tq[2][32][33];  // [y row: 0 = y-1, 1 = y][x - x0][z - z0 + 1]
+  __shared__ float res[32][33];     // [z - z0][x - x0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, py = ny + 2 * m;
+  const int z0 = blockIdx.x * 32, x0 = blockIdx.y * 32, y = blockIdx.z;  // real voxel coordinates
+  for (int e = threadIdx.x; e < 2 * 32 * 33; e += 256) {
+    const int h = e / (32 * 33), f = e % (32 * 33);
+    const int dz = f % 33, dx = f / 33;
+    const int zi = z0 + m - 1 + dz, xi = x0 + m + dx, yi = y + m - 1 + h;  // padded cell coordinates
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zi < pz && x0 + dx < nx) val = q[((long long)xi * py + yi) * pz + zi];
+    tq[h][dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8)
+    res[tz][tx] = tq[1][tx][tz + 1].x + tq[0][tx][tz + 1].y + tq[1][tx][tz].z + tq[0][tx][tz].w;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int dx = e & 31, dz = e >> 5;
+    const int x = x0 + dx, z = z0 + dz;
+    if (x < nx && z < nz) vol[((long long)z * ny + y) * nx + x] += res[dz][dx];
+  }
 }
 
 // vol = fold of the z-fastest scatter quads: the tap at padded (z, y, x) is
@@ -2256,19 +2306,24 @@ static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double 
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
   TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   if (zfast) {
     TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
+    TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
     const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
-    cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.as<float4>(), nx, ny, nz, sx, sy, sz,
-                                                               dviews.as<Fp2View>(), rows, cols, n_views, step);
+    cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.as<float4>(), qB.as<float4>(), nx, ny, nz,
+                                                               sx, sy, sz, dviews.as<Fp2View>(), rows, cols,
+                                                               n_views, step);
     TK_LAUNCHED("cone_fp_adjoint4z_kernel");
     unquad_z_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qA.as<float4>(), nz, ny, nx,
                                                                                  vol);
     TK_LAUNCHED("unquad_z_kernel");
+    unquad_zx_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qB.as<float4>(), nz, ny, nx,
+                                                                                  vol);
+    TK_LAUNCHED("unquad_zx_kernel");
     return TK_OK;
   }
-  TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
   TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
   const long long nblocks = (long long)ceil_div(cols, kFp2BX) * ceil_div(rows, kFp2BY) * n_views;
