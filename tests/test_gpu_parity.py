@@ -227,6 +227,25 @@ class TestAdjoint:
         for g in (gp, gf):
             assert tk.dot_test(tk.forward_projection_op(g, matched=True), trials=4) <= 1e-4
 
+    def test_cfg5_full_size_matched_dot_test(self, tk):
+        """The north star's adjoint test at the cfg5 size (512^3, 720 views, 1024^2,
+        helical over 4 pi): <A x, y> vs <x, A^T y> for the quad-scatter transpose, on a
+        smooth phantom plus noise and on white noise (float64 inner products)."""
+        from paper_2511_08427_b200.projectors import fp_adjoint_tensor, fp_tensor
+
+        mats = tk.helical_trajectory_3d(720, 4 * np.pi, 1200.0, 750.0, (1024, 1024), (0.6, 0.6), -64.0, 64.0)
+        geom = tk.GeometryCone3D((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6), mats, 1200.0, 750.0)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        xs = [tk.phantoms.shepp_logan_3d((512,) * 3) + 0.1 * torch.randn((512,) * 3, device="cuda", generator=g),
+              torch.randn((512,) * 3, device="cuda", generator=g)]
+        for x in xs:
+            y = torch.randn((720, 1024, 1024), device="cuda", generator=g)
+            lhs = float((fp_tensor(x, geom, 0.25).double() * y.double()).sum())
+            rhs = float((x.double() * fp_adjoint_tensor(y, geom, 0.25).double()).sum())
+            assert abs(lhs - rhs) / max(abs(lhs), abs(rhs)) < 1e-4, (lhs, rhs)
+            del y
+            torch.cuda.empty_cache()
+
     def test_matched_equals_oracle_transpose(self, tk, oracle):
         geom = cone(tk, 12, 10, 1.7, 5)
         y = np.random.default_rng(11).standard_normal((5, 10, 10))

@@ -215,3 +215,20 @@ class TestRowBands:
             spans = [D.shard_bounds(n, w, r) for r in range(w)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_tapered_pipeline_chunks_cover_views_once():
+    """ops._tapered: the copy/compute pipelines' view chunks partition [0, n) in
+    order, with the short chunk at the head (H2D pipelines) or tail (D2H)."""
+    from paper_2511_08427_b200.ops import _tapered
+
+    for n in (1, 2, 5, 37, 720, 1001):
+        for parts in (1, 3, 12):
+            for small in (0, 1, 8, 12):
+                for head in (True, False):
+                    ch = _tapered(n, parts, small, head)
+                    assert ch[0][0] == 0 and ch[-1][1] == n
+                    assert all(b < e for b, e in ch) and all(ch[i][1] == ch[i + 1][0] for i in range(len(ch) - 1))
+                    if n > max(1, small):
+                        short = ch[0] if head else ch[-1]
+                        assert short[1] - short[0] == max(1, small)
