@@ -2033,6 +2033,56 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Quad form ("red4", default): one REDG.F32x4 per voxel-view update into a
+// detector quad buffer Qs[v][r0+1][c0+1] += (w00, w01, w10, w11) (one-texel
+// margin so partially covered cells keep their in-detector taps), folded back
+// into the sinogram by unquad_det_kernel.  Same weights and products as
+// cone_bp_adjoint_kernel.
+__global__ void __launch_bounds__(256)
+    cone_bp_adjoint4_kernel(const float *__restrict__ vol, int nx, int ny, int nz, float cx, float cy, float cz,
+                            const ConeVoxView *__restrict__ views, int rows, int cols, float cu, float cv,
+                            float sid, int weighted, float4 *__restrict__ qs) {
+  const long long nvox = (long long)nx * ny * nz;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (i >= nvox) return;
+  const float g = __ldg(vol + i);
+  if (g == 0.f) return;
+  const int ix = (int)(i % nx), iy = (int)((i / nx) % ny), iz = (int)(i / ((long long)nx * ny));
+  const float xc = (float)ix - cx, yc = (float)iy - cy, zc = (float)iz - cz;
+  const ConeVoxView V = views[v];
+  const float w = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc, V.w[3])));
+  if (!(w > (float)kTiny)) return;
+  const float rw = 1.f / w;
+  const float fc = fmaf(fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc, V.a[3]))), rw, cu);
+  const float fr = fmaf(fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc, V.b[3]))), rw, cv);
+  float gg = g;
+  if (weighted) {
+    const float q = sid * rw;
+    gg *= q * q;
+  }
+  const float flc = floorf(fc), flr = floorf(fr);
+  const int c0 = (int)flc, r0 = (int)flr;
+  if (r0 < -1 || r0 >= rows || c0 < -1 || c0 >= cols) return;  // all four taps off the detector
+  const float wc = fc - flc, wr = fr - flr;
+  float4 *e = qs + ((long long)v * (rows + 1) + (r0 + 1)) * (cols + 1) + (c0 + 1);
+  red_add_v4(e, make_float4(gg * (1.f - wr) * (1.f - wc), gg * (1.f - wr) * wc, gg * wr * (1.f - wc), gg * wr * wc));
+}
+
+// sino[v][r][c] = Qs[r+1][c+1].x + Qs[r+1][c].y + Qs[r][c+1].z + Qs[r][c].w
+__global__ void __launch_bounds__(256) unquad_det_kernel(const float4 *__restrict__ qs, int n_views, int rows,
+                                                         int cols, float *__restrict__ sino) {
+  const long long n = (long long)n_views * rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cols);
+    const long long t = i / cols;
+    const int r = (int)(t % rows);
+    const long long v = t / rows;
+    const float4 *row1 = qs + (v * (rows + 1) + (r + 1)) * (cols + 1), *row0 = row1 - (cols + 1);
+    sino[i] = __ldg(row1 + c + 1).x + __ldg(row1 + c).y + __ldg(row0 + c + 1).z + __ldg(row0 + c).w;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host-side packing
 // ---------------------------------------------------------------------------
@@ -2659,9 +2709,25 @@ int tk_back_cone_3d_adjoint(const float *vol, int nz, int ny, int nx, double sz,
   pack_bp_views(mats, n_views, sx, sy, sz, cu, cv, hv, zinv);
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeVoxView) * n_views, st));
-  TK_TRY_CUDA(cudaMemsetAsync(sino_out, 0, sizeof(float) * (size_t)n_views * rows * cols, st));
   const long long nvox = (long long)nx * ny * nz;
   dim3 grid(ceil_div(nvox, 256), n_views);
+  const char *ta = getenv("TK_BPT_ALGO");  // red4 (default: detector quads) | scatter (scalar atomics)
+  if (!(ta && !strcmp(ta, "scatter"))) {
+    Scratch qs;
+    const size_t nq = (size_t)n_views * (rows + 1) * (cols + 1);
+    TK_TRY_CUDA(qs.alloc(sizeof(float4) * nq, st));
+    TK_TRY_CUDA(cudaMemsetAsync(qs.ptr, 0, sizeof(float4) * nq, st));
+    cone_bp_adjoint4_kernel<<<grid, 256, 0, st>>>(vol, nx, ny, nz, (float)((nx - 1) / 2.0), (float)((ny - 1) / 2.0),
+                                                  (float)((nz - 1) / 2.0), dviews.as<ConeVoxView>(), rows, cols,
+                                                  (float)cu, (float)cv, (float)sid, weighted, qs.as<float4>());
+    TK_LAUNCHED("cone_bp_adjoint4_kernel");
+    const long long npix = (long long)n_views * rows * cols;
+    unquad_det_kernel<<<(unsigned)std::min<long long>(ceil_div(npix, 256), (long long)sm_count() * 16), 256, 0, st>>>(
+        qs.as<float4>(), n_views, rows, cols, sino_out);
+    TK_LAUNCHED("unquad_det_kernel");
+    return TK_OK;
+  }
+  TK_TRY_CUDA(cudaMemsetAsync(sino_out, 0, sizeof(float) * (size_t)n_views * rows * cols, st));
   cone_bp_adjoint_kernel<<<grid, 256, 0, st>>>(vol, nx, ny, nz, (float)((nx - 1) / 2.0),
                                                (float)((ny - 1) / 2.0), (float)((nz - 1) / 2.0),
                                                dviews.as<ConeVoxView>(), n_views, rows, cols,

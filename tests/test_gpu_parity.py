@@ -442,6 +442,20 @@ def test_fp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
         assert rel(got, want) < TOL
 
 
+@pytest.mark.parametrize("algo", ["red4", "scatter"])
+def test_bp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
+    monkeypatch.setenv("TK_BPT_ALGO", algo)
+    shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
+    hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
+    x = np.random.default_rng(32).standard_normal(shape)
+    for mats in (hel, tk.circular_trajectory_3d(13, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4))):
+        geom = tk.GeometryCone3D(shape, sp, (30, 34), (1.5, 1.4), mats, 1200.0, 750.0)
+        for w in (False, True):
+            got = tk.transpose_back_project(tk.Volume(x, sp), geom, w).data
+            want = oracle.back_cone_3d_T(x, geom.matrix_array(), 750.0, (30, 34), sp, w)
+            assert rel(got, want) < TOL
+
+
 def _set_bp_algo(monkeypatch, algo):
     if algo == "quad8x1":  # quad kernel with the 8x1 quarter-warp voxel mapping
         monkeypatch.setenv("TK_BP_Q42", "0")
