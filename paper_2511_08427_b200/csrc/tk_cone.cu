@@ -474,8 +474,11 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
 constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
 // RB = detector rows per CTA band (8, 16 or 32): the CTA's 16 quarter-warps
 // cover (128 / RB) columns x RB rows, each quarter 8 consecutive rows of one column.
-template <int MINB, bool COEF, int RB = 8>
-__global__ void __launch_bounds__(128, MINB)
+// VG > 1: one CTA = VG sub-blocks of 128 threads on the SAME detector tile of VG
+// consecutive views (their rays are the previous view's rotated by 2pi/V about
+// the axis, so near the axis they sample the same cells: L1 sharing on one SM).
+template <int MINB, bool COEF, int RB = 8, int VG = 1>
+__global__ void __launch_bounds__(128 * VG, (MINB + VG - 1) / VG)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
                      float *__restrict__ out, unsigned zpitch, unsigned xpitch) {
@@ -485,12 +488,14 @@ __global__ void __launch_bounds__(128, MINB)
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
   const unsigned bt = b / ncb;
-  const int v = (int)(bt % n_views);
-  const int rb = (int)(bt / n_views);
-  const int qd = threadIdx.x >> 3;  // quarter-warp index in the CTA
+  const int nvg = (n_views + VG - 1) / VG;
+  const int v = (int)(bt % nvg) * VG + (int)(threadIdx.x >> 7);
+  const int rb = (int)(bt / nvg);
+  const int t = threadIdx.x & 127;
+  const int qd = t >> 3;  // quarter-warp index in the sub-block
   const int c = cb * kCols + qd / kQpc;
-  const int r = rb * RB + (qd % kQpc) * kFpzRows + (threadIdx.x & 7);
-  if (c >= cols || r >= rows) return;
+  const int r = rb * RB + (qd % kQpc) * kFpzRows + (t & 7);
+  if (c >= cols || r >= rows || v >= n_views) return;
   float *dst = out + ((long long)v * rows + r) * cols + c;
   const Fp2View W = views[v];
   RaySetup rs;
@@ -2257,16 +2262,21 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   } else if (pl.zfast) {
     const char *rbe = getenv("TK_FPZ_RB");  // detector rows per CTA band: 8 (default), 16, 32
     const int rbz = rbe ? atoi(rbe) : 8;
-    const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * n_views;
+    const char *vge = getenv("TK_FPZ_VG");  // consecutive views per CTA: 4 (default), 1, 2, 6
+    const int vgz = rbz != 8 ? 1 : (vge ? atoi(vge) : 4);
+    const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * ceil_div(n_views, vgz);
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)
                         : (minb >= 12 ? cone_fp4z_kernel<12, true>
                                       : (minb >= 10 ? cone_fp4z_kernel<10, true> : cone_fp4z_kernel<8, true>));
     if (!pl.diff && rbz == 16) kern = cone_fp4z_kernel<12, true, 16>;
     if (!pl.diff && rbz == 32) kern = cone_fp4z_kernel<12, true, 32>;
-    kern<<<(unsigned)nbz, 128, 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
-                                        pl.sz, dviews.as<Fp2View>(), rows, cols, n_views, step, out, pl.zpitch,
-                                        pl.xpitch);
+    if (!pl.diff && vgz == 2) kern = cone_fp4z_kernel<12, true, 8, 2>;
+    if (!pl.diff && vgz == 4) kern = cone_fp4z_kernel<12, true, 8, 4>;
+    if (!pl.diff && vgz == 6) kern = cone_fp4z_kernel<12, true, 8, 6>;
+    kern<<<(unsigned)nbz, 128 * (pl.diff ? 1 : vgz), 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny,
+                                                              pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
+                                                              cols, n_views, step, out, pl.zpitch, pl.xpitch);
     TK_LAUNCHED("cone_fp4z_kernel");
   } else if (pl.plane) {
     auto kern = mb && minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;  // 10: no spills (measured best)
