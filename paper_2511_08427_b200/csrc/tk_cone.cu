@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256) quad_volume_z_kernel(const float *__restr
 // sharing between a cell's y+1 row and the next cell's y row: measured 776 ms
 // vs 489 ms.)
 __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
-                                                            float4 *__restrict__ cq, int zpitch, int xpitch) {
+                                                            float4 *__restrict__ cq, int zpitch, long long ystride) {
   __shared__ float tile[33][34];  // [x - x0][z - z0]
   constexpr int m = kFpMargin;
   const int pz = nz + 2 * m, px = nx + 2 * m;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
     const int z = z0 + tz, x = x0 + tx;  // cell (z, y, x) of the padded grid
     if (z + m >= pz || x + m >= px) continue;
     const float v00 = tile[tx][tz], v01 = tile[tx + 1][tz], v10 = tile[tx][tz + 1], v11 = tile[tx + 1][tz + 1];
-    cq[((long long)(y + m) * xpitch + (x + m)) * zpitch + (z + m)] =
+    cq[(long long)(y + m) * ystride + (long long)(x + m) * zpitch + (z + m)] =
         make_float4(v00, v01 - v00, v10 - v00, (v11 - v10) - (v01 - v00));
   }
 }
@@ -477,11 +477,15 @@ constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
 // VG > 1: one CTA = VG sub-blocks of 128 threads on the SAME detector tile of VG
 // consecutive views (their rays are the previous view's rotated by 2pi/V about
 // the axis, so near the axis they sample the same cells: L1 sharing on one SM).
-template <int MINB, bool COEF, int RB = 8, int VG = 1>
+// FIXS: the y stride is the compile-time constant kFpFixS (cells), so the far
+// row's load is the near row's address + an immediate offset (kFpFixS * 16 B
+// fits LDG's signed 24-bit offset): no 64-bit add per load.
+constexpr unsigned kFpFixS = 524032u;  // 2047 * 256 cells: z pitch must be == 255 (mod 256)
+template <int MINB, bool COEF, int RB = 8, int VG = 1, bool FIXS = false>
 __global__ void __launch_bounds__(128 * VG, (MINB + VG - 1) / VG)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
-                     float *__restrict__ out, unsigned zpitch, unsigned xpitch) {
+                     float *__restrict__ out, unsigned zpitch, unsigned ystride) {
   // view-major order within RB-row bands
   constexpr int kCols = 128 / RB, kQpc = RB / kFpzRows;  // columns per CTA, quarters per column
   const int ncb = (cols + kCols - 1) / kCols;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(128 * VG, (MINB + VG - 1) / VG)
   // IMAD.WIDE per address instead of IADD + LEA + LEA.HI.X).  Coordinates are
   // >= 0 here, so floor(f) = bits(f + 2^23) - 0x4B000000.
   const float magic = COEF ? 8388608.f : kFloorMagic;
-  const unsigned sxs = zpitch, sys = xpitch * zpitch;  // x and y strides (cells)
+  const unsigned sxs = zpitch, sys = FIXS ? kFpFixS : ystride;  // x and y strides (cells)
   const unsigned bias = COEF ? 0u : kFloorBits * (1u + sxs + sys);
   unsigned cell = 0xffffffffu;
   float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
@@ -2143,6 +2147,8 @@ struct FpPlan {
   bool plane = false; // b-plane difference quads (ldg4p)
   bool zfast = false; // one z-fastest copy (ldg4z coefficient cells, ldg4zq difference quads)
   unsigned zpitch = 0, xpitch = 0;  // z-fastest cell pitches
+  unsigned ystride = 0;              // cells between rows y and y + 1
+  bool fixs = false;                 // ystride == kFpFixS (immediate-offset far-row loads)
   void *qA = nullptr, *qB = nullptr;
 };
 
@@ -2179,7 +2185,21 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
         }
       }
     }
-    const long long nz_cells = (long long)(ny + m2) * plan->xpitch * plan->zpitch;
+    plan->ystride = plan->xpitch * plan->zpitch;
+    const char *nofix = getenv("TK_FPZ_NOFIX");  // 1: runtime y stride (no immediate-offset far-row loads)
+    if (!plan->diff && !(nofix && atoi(nofix))) {
+      // fixed y stride: z pitch == 255 (mod 256) keeps the floor bias zero
+      // (1 + zp + kFpFixS == 0 mod 256); worth it when the padding is < 2x
+      const unsigned zpf = (unsigned)(nz + m2) + (255u - (unsigned)(nz + m2) % 256u);
+      const unsigned long long xz = (unsigned long long)(nx + m2) * zpf;
+      if (xz <= kFpFixS && 2 * (unsigned long long)(nx + m2) * (nz + m2) >= kFpFixS) {
+        plan->zpitch = zpf;
+        plan->xpitch = (unsigned)(nx + m2);
+        plan->ystride = kFpFixS;
+        plan->fixs = true;
+      }
+    }
+    const long long nz_cells = (long long)(ny + m2) * plan->ystride;
     if (nz_cells >= (1LL << 32)) return fail_arg("tk_forward_cone_3d: volume too large for 32-bit cell indices");
     TK_TRY_CUDA(cudaMallocAsync(&plan->qA, esz * nz_cells, st));
     dim3 tg(ceil_div(nz + 2 * kFpMargin, 32), ceil_div(nx + 2 * kFpMargin, 32), ny + 2 * kFpMargin);
@@ -2188,7 +2208,7 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       TK_LAUNCHED("quad_volume_z_kernel");
     } else {  // coefficient cells (ldg4z)
       coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA), (int)plan->zpitch,
-                                               (int)plan->xpitch);
+                                               (long long)plan->ystride);
       TK_LAUNCHED("coef_volume_z_kernel");
     }
     return TK_OK;
@@ -2272,11 +2292,11 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     if (!pl.diff && rbz == 16) kern = cone_fp4z_kernel<12, true, 16>;
     if (!pl.diff && rbz == 32) kern = cone_fp4z_kernel<12, true, 32>;
     if (!pl.diff && vgz == 2) kern = cone_fp4z_kernel<12, true, 8, 2>;
-    if (!pl.diff && vgz == 4) kern = cone_fp4z_kernel<12, true, 8, 4>;
+    if (!pl.diff && vgz == 4) kern = pl.fixs ? cone_fp4z_kernel<12, true, 8, 4, true> : cone_fp4z_kernel<12, true, 8, 4>;
     if (!pl.diff && vgz == 6) kern = cone_fp4z_kernel<12, true, 8, 6>;
     kern<<<(unsigned)nbz, 128 * (pl.diff ? 1 : vgz), 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny,
                                                               pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
-                                                              cols, n_views, step, out, pl.zpitch, pl.xpitch);
+                                                              cols, n_views, step, out, pl.zpitch, pl.ystride);
     TK_LAUNCHED("cone_fp4z_kernel");
   } else if (pl.plane) {
     auto kern = mb && minb >= 12 ? cone_fp4p_kernel<12> : cone_fp4p_kernel<10>;  // 10: no spills (measured best)
