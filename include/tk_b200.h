@@ -169,6 +169,34 @@ int tk_fft_filter_rows_ex(const float *in, long long n_rows, int width, int band
 /* out[i] = in[i] * scale (fp32), n elements; in/out may alias. */
 int tk_scale(const float *in, long long n, double scale, float *out, void *stream);
 
+/* ---- sinogram degradation simulators (reference artifacts.py:50-211) ----
+ * Elementwise / small-stencil kernels on device sinograms (n_views, rows, cols)
+ * (rows = 1 for 2D).  Noise comes from a counter-based Philox4x32-10 stream
+ * per (seed, view), indexed by texel: reproducible for a seed, independent of
+ * launch configuration; the distributions are the contract (artifacts.py:5-7).
+ * out may not alias sino. */
+/* the per-view integer offsets tk_detector_jitter draws, uniform in [-max, max] (host) */
+int tk_jitter_shifts(unsigned long long seed, int n_views, int max_shift, int *shifts_out);
+/* add_detector_jitter (artifacts.py:50-66): shift each view by its offset along
+ * u (axis_v = 0) or v (axis_v = 1), zero-filling the vacated strip */
+int tk_detector_jitter(const float *sino, int n_views, int rows, int cols, int axis_v, int max_shift,
+                       unsigned long long seed, float *out, void *stream);
+/* add_poisson_noise (artifacts.py:69-93): transmission = 1: -ln(max(Poisson(i0 e^-p), 1) / i0);
+ * transmission = 0: Poisson(p) (direct mode) */
+int tk_poisson_noise(const float *sino, int n_views, long long view_size, double i0, int transmission,
+                     unsigned long long seed, float *out, void *stream);
+/* add_gaussian_noise (artifacts.py:96-105): p + mean + std N(0, 1) */
+int tk_gaussian_noise(const float *sino, int n_views, long long view_size, double mean, double std,
+                      unsigned long long seed, float *out, void *stream);
+/* add_ring_artifact (artifacts.py:108-146): host columns[n_columns]; views [start, end);
+ * zero = 1 clears them, zero = 0 multiplies by factor; everything else copied bit-exact */
+int tk_ring_artifact(const float *sino, int n_views, int rows, int cols, const int *columns, int n_columns,
+                     int start, int end, int zero, double factor, float *out, void *stream);
+/* add_gantry_motion_blur (artifacts.py:183-211): zero-padded 2D convolution of view i with
+ * the host float64 kernel kernels[i][2 half + 1][2 half + 1] (rows: v, columns: u) */
+int tk_gantry_blur(const float *sino, int n_views, int rows, int cols, const double *kernels, int half,
+                   float *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,5 +36,8 @@ from .projectors import (SamplingConfig, back_project, back_project_cone_3d, bac
                          transpose_back_project, transpose_forward_project)
 
 from . import phantoms  # noqa: E402  (synthetic inputs on the GPU)
+from . import artifacts  # noqa: E402  (sinogram degradation simulators, reference artifacts.py)
+from .artifacts import (add_detector_jitter, add_gantry_motion_blur, add_gaussian_noise,  # noqa: E402
+                        add_poisson_noise, add_ring_artifact)
 
 __version__ = "0.1.0"

@@ -64,6 +64,14 @@ SIGNATURES = {
     "tk_fft_filter_rows_ex": [_ptr, _c_ll, _c_int, _c_int, _c_int, _c_int, _dptr, _c_int, _c_dbl,
                               _c_dbl, _c_dbl, _c_dbl, _ptr, _ptr],
     "tk_scale": [_ptr, _c_ll, _c_dbl, _ptr, _ptr],
+    # sinogram degradation simulators (artifacts.py)
+    "tk_jitter_shifts": [ctypes.c_ulonglong, _c_int, _c_int, ctypes.POINTER(ctypes.c_int)],
+    "tk_detector_jitter": [_ptr, _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_ulonglong, _ptr, _ptr],
+    "tk_poisson_noise": [_ptr, _c_int, _c_ll, _c_dbl, _c_int, ctypes.c_ulonglong, _ptr, _ptr],
+    "tk_gaussian_noise": [_ptr, _c_int, _c_ll, _c_dbl, _c_dbl, ctypes.c_ulonglong, _ptr, _ptr],
+    "tk_ring_artifact": [_ptr, _c_int, _c_int, _c_int, ctypes.POINTER(ctypes.c_int), _c_int, _c_int, _c_int,
+                         _c_int, _c_dbl, _ptr, _ptr],
+    "tk_gantry_blur": [_ptr, _c_int, _c_int, _c_int, _dptr, _c_int, _ptr, _ptr],
 }
 
 _lock = threading.Lock()
