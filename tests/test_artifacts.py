@@ -238,3 +238,26 @@ class TestRingAndBlur:
                     tk.add_detector_jitter(s, 2, "u", seed=1), tk.add_ring_artifact(s, [100, 500], None, "zero"),
                     tk.add_gantry_motion_blur(s, geom, 5)):
             assert out.data.shape == s.data.shape and bool(torch.isfinite(out.data).all())
+
+
+@pytest.mark.gpu
+def test_config_artifact_chain(tk, rng):
+    """PipelineConfig.apply_artifacts runs the reference's chain schema (config.py:208-258)."""
+    from paper_2511_08427_b200.config import ConfigError, PipelineConfig
+
+    base = {"geometry_kind": "cone3d", "volume_shape": [16, 16, 16], "volume_spacing": [1, 1, 1],
+            "detector_shape": [20, 24], "detector_spacing": [1.0, 1.0], "number_of_projections": 6,
+            "angular_range": 2 * np.pi, "sdd": 1200.0, "sid": 750.0}
+    chain = [{"kind": "poisson", "i0": 1e5, "seed": 3}, {"kind": "ring", "columns": [2], "mode": "zero"},
+             {"kind": "gantry_blur", "kernel_len_px": 3}, {"kind": "gaussian", "std": 0.0, "mean": 0.5}]
+    cfg = PipelineConfig.from_dict({**base, "artifacts": chain})
+    geom = cfg.build_geometry()
+    s = sino3d(rng)
+    out = cfg.apply_artifacts(s, geom)
+    want = tk.add_gaussian_noise(tk.add_gantry_motion_blur(tk.add_ring_artifact(
+        tk.add_poisson_noise(s, 1e5, seed=3), [2]), geom, 3), 0.5, 0.0)
+    assert torch.equal(out.data, want.data)
+    for bad in ([{"kind": "nope"}], [{"kind": "poisson"}], [{"kind": "gaussian", "std": 1.0, "extra": 1}],
+                [{"kind": "poisson", "i0": -1.0}]):
+        with pytest.raises(ConfigError):
+            PipelineConfig.from_dict({**base, "artifacts": bad}).apply_artifacts(s, geom)
