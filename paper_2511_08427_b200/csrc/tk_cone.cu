@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(256) quad_volume_z_kernel(const float *__restr
 // sharing between a cell's y+1 row and the next cell's y row: measured 776 ms
 // vs 489 ms.)
 __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
-                                                            float4 *__restrict__ cq, int zpitch, long long ystride) {
+                                                            float4 *__restrict__ cq, int zpitch, long long ystride,
+                                                            int acbd) {
   __shared__ float tile[33][34];  // [x - x0][z - z0]
   constexpr int m = kFpMargin;
   const int pz = nz + 2 * m, px = nx + 2 * m;
@@ -466,9 +467,39 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
     const int z = z0 + tz, x = x0 + tx;  // cell (z, y, x) of the padded grid
     if (z + m >= pz || x + m >= px) continue;
     const float v00 = tile[tx][tz], v01 = tile[tx + 1][tz], v10 = tile[tx][tz + 1], v11 = tile[tx + 1][tz + 1];
+    const float A = v00, B = v01 - v00, C = v10 - v00, D = (v11 - v10) - (v01 - v00);
+    // acbd: (A, C, B, D) so that (A, C) and (B, D) are register pairs for FFMA2
     cq[(long long)(y + m) * ystride + (long long)(x + m) * zpitch + (z + m)] =
-        make_float4(v00, v01 - v00, v10 - v00, (v11 - v10) - (v01 - v00));
+        acbd ? make_float4(A, C, B, D) : make_float4(A, B, C, D);
   }
+}
+
+// Packed fp32 pairs (sm_100a FFMA2 / FADD2: two fp32 FMAs / adds per
+// instruction, operand-selectable halves and broadcast scalars).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2_rm(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
 constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
@@ -481,7 +512,7 @@ constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
 // row's load is the near row's address + an immediate offset (kFpFixS * 16 B
 // fits LDG's signed 24-bit offset): no 64-bit add per load.
 constexpr unsigned kFpFixS = 524032u;  // 2047 * 256 cells: z pitch must be == 255 (mod 256)
-template <int MINB, bool COEF, int RB = 8, int VG = 1, bool FIXS = false>
+template <int MINB, bool COEF, int RB = 8, int VG = 1, bool FIXS = false, bool F2 = false>
 __global__ void __launch_bounds__(128 * VG, (MINB + VG - 1) / VG)
     cone_fp4z_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                      const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
@@ -519,7 +550,28 @@ __global__ void __launch_bounds__(128 * VG, (MINB + VG - 1) / VG)
   const unsigned bias = COEF ? 0u : kFloorBits * (1u + sxs + sys);
   unsigned cell = 0xffffffffu;
   float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
+  const unsigned long long e2 = pk2(ex, ey), g2 = pk2(gx, gy), m2 = pk2(magic, magic);
   auto sample = [&](float kk) -> float {
+    if (F2) {  // (x, y) as FFMA2 / FADD2 pairs; cells stored (A, C, B, D); bit-identical results
+      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
+      const float fz = fmaf(kk, gz, ez);
+      const unsigned long long xxy = fadd2_rm(fxy, m2);
+      const float xz = __fadd_rd(fz, magic);
+      const float2 xb = upk2(xxy);
+      const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * sxs + __float_as_uint(xz));
+      if (id != cell) {
+        cell = id;
+        const float4 *p = elem_ptr(q, id - bias);
+        lo4 = __ldg(p);
+        hi4 = __ldg(p + sys);
+      }
+      const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
+      const float wz = fz - (xz - magic);
+      const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
+      const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
+      const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
+      return lerpf(s0, s1, w.y);
+    }
     const float fx = fmaf(kk, gx, ex), fy = fmaf(kk, gy, ey), fz = fmaf(kk, gz, ez);
     const float xx = __fadd_rd(fx, magic), xy = __fadd_rd(fy, magic), xz = __fadd_rd(fz, magic);
     const unsigned id = __float_as_uint(xy) * sys + (__float_as_uint(xx) * sxs + __float_as_uint(xz));
@@ -2148,6 +2200,7 @@ struct FpPlan {
   bool zfast = false; // one z-fastest copy (ldg4z coefficient cells, ldg4zq difference quads)
   unsigned zpitch = 0, xpitch = 0;  // z-fastest cell pitches
   unsigned ystride = 0;              // cells between rows y and y + 1
+  bool f2 = false;                   // cells stored (A, C, B, D) for the FFMA2 march
   bool fixs = false;                 // ystride == kFpFixS (immediate-offset far-row loads)
   void *qA = nullptr, *qB = nullptr;
 };
@@ -2207,8 +2260,10 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       quad_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA));
       TK_LAUNCHED("quad_volume_z_kernel");
     } else {  // coefficient cells (ldg4z)
+      const char *f2e = getenv("TK_FPZ_F2");  // 1 (default): FFMA2 / FADD2 pair march
+      plan->f2 = plan->fixs && !(f2e && !atoi(f2e));
       coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA), (int)plan->zpitch,
-                                               (long long)plan->ystride);
+                                               (long long)plan->ystride, plan->f2 ? 1 : 0);
       TK_LAUNCHED("coef_volume_z_kernel");
     }
     return TK_OK;
@@ -2292,7 +2347,9 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     if (!pl.diff && rbz == 16) kern = cone_fp4z_kernel<12, true, 16>;
     if (!pl.diff && rbz == 32) kern = cone_fp4z_kernel<12, true, 32>;
     if (!pl.diff && vgz == 2) kern = cone_fp4z_kernel<12, true, 8, 2>;
-    if (!pl.diff && vgz == 4) kern = pl.fixs ? cone_fp4z_kernel<12, true, 8, 4, true> : cone_fp4z_kernel<12, true, 8, 4>;
+    if (!pl.diff && vgz == 4)
+      kern = pl.f2 ? cone_fp4z_kernel<12, true, 8, 4, true, true>
+                   : (pl.fixs ? cone_fp4z_kernel<12, true, 8, 4, true> : cone_fp4z_kernel<12, true, 8, 4>);
     if (!pl.diff && vgz == 6) kern = cone_fp4z_kernel<12, true, 8, 6>;
     kern<<<(unsigned)nbz, 128 * (pl.diff ? 1 : vgz), 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny,
                                                               pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
