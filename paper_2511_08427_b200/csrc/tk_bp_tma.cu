@@ -132,9 +132,20 @@ __global__ void __launch_bounds__(kBtThreads, 2)
   const bool active = ix < p.nx && iy < p.ny;
   const float xc = (float)ix - p.cx, yc = (float)iy - p.cy;
   const float zc0 = (float)(p.z_begin + zl0) - p.cz;
-  float acc[kBtZB];
+  // accumulators as packed pairs (z-voxels 2j, 2j+1): the per-update arithmetic
+  // runs as FFMA2 / FADD2 / FMUL2 on two voxels at once (same operations and
+  // rounding as the scalar form, half the instructions)
+  unsigned long long accp[kBtZB / 2];
 #pragma unroll
-  for (int k = 0; k < kBtZB; ++k) acc[k] = 0.f;
+  for (int j = 0; j < kBtZB / 2; ++j) accp[j] = 0ull;
+  auto add_acc = [&](int k, float val) {
+    float2 a = upk2(accp[k >> 1]);
+    if (k & 1)
+      a.y += val;
+    else
+      a.x += val;
+    accp[k >> 1] = pk2(a.x, a.y);
+  };
 
   for (int v = 0; v < p.n_views; ++v) {
     const int s = v % kBtStages;
@@ -162,14 +173,21 @@ __global__ void __launch_bounds__(kBtThreads, 2)
         const float *t = bt_tiles + (size_t)s * stage_floats +
                          ((int)(__float_as_uint(xcf) - kFloorBits) - m.c0);
         const int rbias = (int)kFloorBits + m.r0;
+        const unsigned long long drp = pk2(dr, dr), fr0p = pk2(fr0, fr0), g0p = pk2(g0, g0), g1p = pk2(g1, g1);
+        const unsigned long long mg = pk2(kFloorMagic, kFloorMagic);
 #pragma unroll
-        for (int k = 0; k < kBtZB; ++k) {
-          const float fr = fmaf((float)k, dr, fr0);
-          const float xr = floor_magic(fr);
-          const float *e = t + ((int)__float_as_uint(xr) - rbias) * bw;
-          const float top = fmaf(g1, e[1], g0 * e[0]);
-          const float bot = fmaf(g1, e[bw + 1], g0 * e[bw]);
-          acc[k] += fmaf(fr - (xr - kFloorMagic), bot - top, top);
+        for (int j = 0; j < kBtZB / 2; ++j) {
+          const unsigned long long frp = ffma2(pk2((float)(2 * j), (float)(2 * j + 1)), drp, fr0p);
+          const unsigned long long xrp = fadd2_rm(frp, mg);  // floor_magic of both rows
+          const float2 xr = upk2(xrp);
+          const float *ea = t + ((int)__float_as_uint(xr.x) - rbias) * bw;
+          const float *eb = t + ((int)__float_as_uint(xr.y) - rbias) * bw;
+          const unsigned long long e0 = pk2(ea[0], eb[0]), e1 = pk2(ea[1], eb[1]);
+          const unsigned long long e2 = pk2(ea[bw], eb[bw]), e3 = pk2(ea[bw + 1], eb[bw + 1]);
+          const unsigned long long top = ffma2(g1p, e1, fmul2(g0p, e0));
+          const unsigned long long bot = ffma2(g1p, e3, fmul2(g0p, e2));
+          const unsigned long long frac = fsub2(frp, fsub2(xrp, mg));
+          accp[j] = fadd2(accp[j], ffma2(frac, fsub2(bot, top), top));
         }
       } else {  // rectangle exceeds the TMA box: bounded global gathers
         const float *sv = p.sino + (long long)v * p.view_stride;
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
           const float t11 = (rb && cb) ? __ldg(e + p.cols + 1) : 0.f;
           const float top = fmaf(g1, t01, g0 * t00);
           const float bot = fmaf(g1, t11, g0 * t10);
-          acc[k] += fmaf(fr - flr, bot - top, top);
+          add_acc(k, fmaf(fr - flr, bot - top, top));
         }
       }
     }
@@ -200,8 +218,10 @@ __global__ void __launch_bounds__(kBtThreads, 2)
   for (int k = 0; k < kBtZB; ++k) {
     const int zl = zl0 + k;
     if (zl < p.z_count) {
+      const float2 a = upk2(accp[k >> 1]);
+      const float ak = (k & 1) ? a.y : a.x;
       float *o = p.out + ((long long)zl * p.ny + iy) * p.nx + ix;
-      *o = p.accumulate ? *o + acc[k] : acc[k];
+      *o = p.accumulate ? *o + ak : ak;
     }
   }
 }

@@ -474,34 +474,6 @@ __global__ void __launch_bounds__(256) coef_volume_z_kernel(const float *__restr
   }
 }
 
-// Packed fp32 pairs (sm_100a FFMA2 / FADD2: two fp32 FMAs / adds per
-// instruction, operand-selectable halves and broadcast scalars).
-__device__ __forceinline__ unsigned long long pk2(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 upk2(unsigned long long r) {
-  float2 v;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-  return v;
-}
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ unsigned long long fadd2_rm(unsigned long long a, unsigned long long b) {
-  unsigned long long d;
-  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
 constexpr int kFpzRows = 8;  // rows per quarter-warp group (one column)
 // RB = detector rows per CTA band (8, 16 or 32): the CTA's 16 quarter-warps
 // cover (128 / RB) columns x RB rows, each quarter 8 consecutive rows of one column.
