@@ -2309,8 +2309,9 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
   } else if (pl.zfast) {
     const char *rbe = getenv("TK_FPZ_RB");  // detector rows per CTA band: 8 (default), 16, 32
     const int rbz = rbe ? atoi(rbe) : 8;
-    const char *vge = getenv("TK_FPZ_VG");  // consecutive views per CTA: 4 (default), 1, 2, 6
-    const int vgz = rbz != 8 ? 1 : (vge ? atoi(vge) : 4);
+    const char *vge = getenv("TK_FPZ_VG");  // consecutive views per CTA: 4 (default), 1, 2, 6, 8
+    // default: 8 views per CTA for long orbits (0.7 % over 4 at cfg4), 4 for short view blocks
+    const int vgz = rbz != 8 ? 1 : (vge ? atoi(vge) : (pl.f2 && n_views >= 128 ? 8 : 4));
     const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * ceil_div(n_views, vgz);
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)
@@ -2325,6 +2326,8 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
                                          : cone_fp4z_kernel<16, true, 8, 4, true, true>)
                    : (pl.fixs ? cone_fp4z_kernel<12, true, 8, 4, true> : cone_fp4z_kernel<12, true, 8, 4>);
     if (!pl.diff && vgz == 6) kern = cone_fp4z_kernel<12, true, 8, 6>;
+    if (pl.f2 && vgz == 8) kern = cone_fp4z_kernel<16, true, 8, 8, true, true>;
+    if (pl.f2 && vgz == 2) kern = cone_fp4z_kernel<16, true, 8, 2, true, true>;
     kern<<<(unsigned)nbz, 128 * (pl.diff ? 1 : vgz), 0, st>>>(static_cast<const float4 *>(pl.qA), pl.nx, pl.ny,
                                                               pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<Fp2View>(), rows,
                                                               cols, n_views, step, out, pl.zpitch, pl.ystride);
