@@ -127,8 +127,12 @@ __global__ void __launch_bounds__(kBtThreads, 2)
   }
 
   // ---------------- consumer warps: one (x, y) column x kBtZB z-voxels per thread ----------------
-  const int ix = blockIdx.x * kBtTX + (tid & (kBtTX - 1));
-  const int iy = blockIdx.y * kBtTY + tid / kBtTX;
+  // warp = 8 (x) x 4 (y) voxel columns: its taps cover a compact ~11 x 2-4 patch of
+  // the tile, and with a row pitch bw == 12 or 20 (mod 32) the rows it touches fall
+  // in disjoint banks -- 1.02 LDS wavefronts per warp instruction instead of 1.37
+  // for 16 x 2 warps (scripts/bp_bank_model.py)
+  const int ix = blockIdx.x * kBtTX + (warp & 1) * 8 + (lane & 7);
+  const int iy = blockIdx.y * kBtTY + (warp >> 1) * 4 + (lane >> 3);
   const bool active = ix < p.nx && iy < p.ny;
   const float xc = (float)ix - p.cx, yc = (float)iy - p.cy;
   const float zc0 = (float)(p.z_begin + zl0) - p.cz;
@@ -289,7 +293,9 @@ static void footprint_box(const BpParams &p, const ConeVoxView *hv, int kBtZB, i
         }
   }
   bw = ((wmax + 3 + 2 + 3) / 4) * 4;  // +3 for the 16-byte aligned start column, +2 slack
-  if (bw % 32 == 0) bw += 4;  // row pitch off the 32-bank period (a pitch of 24..28 mod 32 measured no better)
+  // row pitch == 12 or 20 (mod 32): adjacent tile rows shift by 12 / 20 banks, so
+  // an 8 x 4 warp's taps on neighbouring rows do not collide (bp_bank_model.py)
+  while (bw % 32 != 12 && bw % 32 != 20) bw += 4;
   bh = hmax + 2;
 }
 
