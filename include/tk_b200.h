@@ -128,6 +128,12 @@ int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int col
                                int nz, int ny, int nx, double sz, double sy,
                                double sx, double step, float *vol_out,
                                void *stream);
+/* As tk_forward_cone_3d_adjoint; deterministic = 1 accumulates in 64-bit fixed point
+ * (scale 2^e from max |sino|, integer atomics): bit-reproducible, ~5x slower. */
+int tk_forward_cone_3d_adjoint_ex(const float *sino, int n_views, int rows, int cols,
+                                  const double *sources, const double *minv, int nz, int ny,
+                                  int nx, double sz, double sy, double sx, double step,
+                                  int deterministic, float *vol_out, void *stream);
 int tk_back_cone_3d_adjoint(const float *vol, int nz, int ny, int nx, double sz,
                             double sy, double sx, const double *mats, double sid,
                             int weighted, int n_views, int rows, int cols,

@@ -53,6 +53,8 @@ SIGNATURES = {
                            _ptr, _ptr],
     "tk_forward_cone_3d_adjoint": [_ptr, _c_int, _c_int, _c_int, _dptr, _dptr, _c_int, _c_int,
                                    _c_int, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _ptr, _ptr],
+    "tk_forward_cone_3d_adjoint_ex": [_ptr, _c_int, _c_int, _c_int, _dptr, _dptr, _c_int, _c_int,
+                                      _c_int, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_int, _ptr, _ptr],
     "tk_back_cone_3d_adjoint": [_ptr, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl, _dptr,
                                 _c_dbl, _c_int, _c_int, _c_int, _c_int, _ptr, _ptr],
     "tk_forward_parallel_2d_adjoint": [_ptr, _c_int, _c_int, _dptr, _dptr, _c_dbl, _c_dbl, _c_int,

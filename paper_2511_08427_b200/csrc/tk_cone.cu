@@ -1165,11 +1165,23 @@ __global__ void __launch_bounds__(256) unquad_tiled_kernel(const float4 *__restr
 // is the old cell's far row: that quad's accumulator is carried over in
 // registers and only the row left behind is flushed (one REDG.F32x4 instead of
 // two).
-template <int MINB>
+// DET: fixed-point flush -- each quad component is rounded to an integer multiple of
+// 2^-e (scale = 2^e, exact) and added with 64-bit integer atomics into u64 quads.
+// Integer addition is associative, so the result does not depend on the order in
+// which rays flush: bit-reproducible (torch.use_deterministic_algorithms).
+__device__ __forceinline__ void red_add_fx4(unsigned long long *p, const float4 &v, float scale) {
+  atomicAdd(p, (unsigned long long)__float2ll_rn(v.x * scale));
+  atomicAdd(p + 1, (unsigned long long)__float2ll_rn(v.y * scale));
+  atomicAdd(p + 2, (unsigned long long)__float2ll_rn(v.z * scale));
+  atomicAdd(p + 3, (unsigned long long)__float2ll_rn(v.w * scale));
+}
+
+template <int MINB, bool DET = false>
 __global__ void __launch_bounds__(128, MINB)
-    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, float4 *__restrict__ qy, float4 *__restrict__ qx,
+    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, void *__restrict__ qy_, void *__restrict__ qx_,
                              int nx, int ny, int nz, double sx, double sy, double sz,
-                             const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step) {
+                             const Fp2View *__restrict__ views, int rows, int cols, int n_views, double step,
+                             float scale) {
   constexpr int kCols = 16;
   const int ncb = (cols + kCols - 1) / kCols;
   const unsigned b = blockIdx.x;
@@ -1187,7 +1199,13 @@ __global__ void __launch_bounds__(128, MINB)
   RaySetup rs;
   if (!cone_ray_setup(W.ray, r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
   const bool xrow = fabsf(rs.gx) > fabsf(rs.gy);  // major horizontal axis (cells per step)
-  float4 *q = xrow ? qx : qy;
+  void *qv = xrow ? qx_ : qy_;
+  auto flush = [&](unsigned cidx, const float4 &v) {  // quad cidx += v
+    if (DET)
+      red_add_fx4(static_cast<unsigned long long *>(qv) + 4ull * cidx, v, scale);
+    else
+      red_add_v4(static_cast<float4 *>(qv) + cidx, v);
+  };
   const float ea = (xrow ? rs.ey : rs.ex) + (kFpMargin - 1), eb = (xrow ? rs.ex : rs.ey) + (kFpMargin - 1);
   const float ez = rs.ez + (kFpMargin - 1);
   const float ga = xrow ? rs.gy : rs.gx, gb = xrow ? rs.gx : rs.gy, gz = rs.gz;
@@ -1205,19 +1223,19 @@ __global__ void __launch_bounds__(128, MINB)
     if (id != cell) {
       const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
       if (open) {
-        float4 *p = q + (cell - bias);
+        const unsigned c0 = cell - bias;
         const unsigned d = id - cell;
         if (d == sbs) {  // row b -> b + 1: the far row becomes the near row
-          red_add_v4(p, lo);
+          flush(c0, lo);
           lo = hi;
           hi = zero;
         } else if (d == 0u - sbs) {  // row b -> b - 1: the near row becomes the far row
-          red_add_v4(p + sbs, hi);
+          flush(c0 + sbs, hi);
           hi = lo;
           lo = zero;
         } else {
-          red_add_v4(p, lo);
-          red_add_v4(p + sbs, hi);
+          flush(c0, lo);
+          flush(c0 + sbs, hi);
           lo = hi = zero;
         }
       }
@@ -1241,9 +1259,37 @@ __global__ void __launch_bounds__(128, MINB)
   const int nfull = rs.n - 1;
   for (int k = 0; k < nfull; ++k, kf += 1.f) sample(kf, g);
   sample((float)nfull + 0.5f * rs.last, g * rs.last);
-  float4 *p = q + (cell - bias);
-  red_add_v4(p, lo);
-  red_add_v4(p + sbs, hi);
+  flush(cell - bias, lo);
+  flush(cell - bias + sbs, hi);
+}
+
+// deterministic fold: vol[z][y][x] = 2^-e (sum of the 8 fixed-point taps of both
+// scatter buffers) -- integer sums, one rounding to float
+__global__ void __launch_bounds__(256) unquad_fx_kernel(const unsigned long long *__restrict__ qy,
+                                                        const unsigned long long *__restrict__ qx, int nz, int ny,
+                                                        int nx, double inv_scale, float *__restrict__ vol) {
+  constexpr int m = kFpMargin;
+  const long long pz = nz + 2 * m, px = nx + 2 * m, py = ny + 2 * m;
+  const long long n = (long long)nz * ny * nx;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long long)nx * ny));
+    const long long zp = z + m, yp = y + m, xp = x + m;
+    // qy: Qz[y][x][z] taps (z,x),(z,x+1),(z+1,x),(z+1,x+1) of row y
+    auto Y = [&](long long yy, long long xx, long long zz, int c) { return (long long)qy[4 * ((yy * px + xx) * pz + zz) + c]; };
+    // qx: Qx[x][y][z] taps (z,y),(z,y+1),(z+1,y),(z+1,y+1) of row x
+    auto X = [&](long long xx, long long yy, long long zz, int c) { return (long long)qx[4 * ((xx * py + yy) * pz + zz) + c]; };
+    const long long t = Y(yp, xp, zp, 0) + Y(yp, xp - 1, zp, 1) + Y(yp, xp, zp - 1, 2) + Y(yp, xp - 1, zp - 1, 3) +
+                        X(xp, yp, zp, 0) + X(xp, yp - 1, zp, 1) + X(xp, yp, zp - 1, 2) + X(xp, yp - 1, zp - 1, 3);
+    vol[i] = (float)((double)t * inv_scale);
+  }
+}
+
+__global__ void absmax_kernel(const float *__restrict__ x, long long n, unsigned *__restrict__ out) {
+  unsigned m = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(__ldg(x + i))));  // non-negative floats order as integers
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // vol += fold of the x-row scatter quads qx: the tap at padded (z, y, x) is
@@ -2410,15 +2456,60 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
 }
 
 // A^T y by quad scatter (cone_fp_adjoint4_kernel) + fold (unquad_tiled_kernel).
+// Deterministic A^T: fixed-point scale 2^e from max |y| so that no tap sum can
+// overflow int64 (contribution <= |y| step, < 512 V contributions per tap).
+static int launch_fp_adjoint_det(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
+                                 const std::vector<Fp2View> &hv, Scratch &dviews, int n_views, int rows, int cols,
+                                 double step, float *vol, cudaStream_t st) {
+  constexpr int m2 = 2 * kFpMargin;
+  const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  const long long nsino = (long long)n_views * rows * cols;
+  Scratch dmax, qA, qB;
+  TK_TRY_CUDA(dmax.alloc(sizeof(unsigned), st));
+  TK_TRY_CUDA(cudaMemsetAsync(dmax.ptr, 0, sizeof(unsigned), st));
+  absmax_kernel<<<(unsigned)std::min<long long>(ceil_div(nsino, 256), (long long)sm_count() * 8), 256, 0, st>>>(
+      sino, nsino, dmax.as<unsigned>());
+  TK_LAUNCHED("absmax_kernel");
+  unsigned bits = 0;
+  TK_TRY_CUDA(cudaMemcpyAsync(&bits, dmax.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  TK_TRY_CUDA(cudaStreamSynchronize(st));
+  float ymax;
+  std::memcpy(&ymax, &bits, sizeof(float));
+  if (!(ymax > 0.f) || !std::isfinite(ymax)) {
+    TK_TRY_CUDA(cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nz * ny * nx, st));
+    return std::isfinite(ymax) ? TK_OK : fail_arg("tk_forward_cone_3d_adjoint: non-finite sinogram");
+  }
+  const double bound = (double)ymax * step * 512.0 * n_views;
+  const int e = std::min(100, (int)std::floor(62.0 - std::log2(bound)));
+  const float scale = std::ldexp(1.0f, e);
+  TK_TRY_CUDA(qA.alloc(32 * ncell, st));
+  TK_TRY_CUDA(qB.alloc(32 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, 32 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, 32 * ncell, st));
+  const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+  if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  cone_fp_adjoint4z_kernel<8, true><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
+                                                                   dviews.as<Fp2View>(), rows, cols, n_views, step,
+                                                                   scale);
+  TK_LAUNCHED("cone_fp_adjoint4z_kernel");
+  const long long nv = (long long)nz * ny * nx;
+  unquad_fx_kernel<<<(unsigned)std::min<long long>(ceil_div(nv, 256), (long long)sm_count() * 16), 256, 0, st>>>(
+      qA.as<unsigned long long>(), qB.as<unsigned long long>(), nz, ny, nx, std::ldexp(1.0, -e), vol);
+  TK_LAUNCHED("unquad_fx_kernel");
+  return TK_OK;
+}
+
 static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
                               const double *sources, const double *minv, int n_views, int rows, int cols,
-                              double step, float *vol, cudaStream_t st, bool zfast) {
+                              double step, float *vol, cudaStream_t st, bool zfast, bool deterministic = false) {
   const std::vector<Fp2View> hv = fp2_views(sources, minv, n_views, sx, sy);
   Scratch dviews, qA, qB;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(Fp2View) * n_views, st));
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
+  if (deterministic)
+    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, hv, dviews, n_views, rows, cols, step, vol, st);
   TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   if (zfast) {
@@ -2426,9 +2517,8 @@ static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double 
     TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
     const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
-    cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.as<float4>(), qB.as<float4>(), nx, ny, nz,
-                                                               sx, sy, sz, dviews.as<Fp2View>(), rows, cols,
-                                                               n_views, step);
+    cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
+                                                               dviews.as<Fp2View>(), rows, cols, n_views, step, 1.f);
     TK_LAUNCHED("cone_fp_adjoint4z_kernel");
     unquad_z_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qA.as<float4>(), nz, ny, nx,
                                                                                  vol);
@@ -2666,6 +2756,21 @@ int tk_fp_plan_destroy(void *plan, void *stream) {
   fp_plan_free(pl, as_stream(stream));
   delete pl;
   return TK_OK;
+}
+
+int tk_forward_cone_3d_adjoint_ex(const float *sino, int n_views, int rows, int cols, const double *sources,
+                                  const double *minv, int nz, int ny, int nx, double sz, double sy, double sx,
+                                  double step, int deterministic, float *vol_out, void *stream) {
+  clear_error();
+  if (!deterministic)
+    return tk_forward_cone_3d_adjoint(sino, n_views, rows, cols, sources, minv, nz, ny, nx, sz, sy, sx, step,
+                                      vol_out, stream);
+  if (!sino || !vol_out || !sources || !minv) return fail_arg("tk_forward_cone_3d_adjoint: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_forward_cone_3d_adjoint: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0 && step > 0)) return fail_arg("tk_forward_cone_3d_adjoint: spacing/step must be > 0");
+  return launch_fp_adjoint4(sino, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, vol_out,
+                            as_stream(stream), true, true);
 }
 
 int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int cols,

@@ -233,9 +233,15 @@ def bp_cone_tensor_ex(sino_band: torch.Tensor, geom: GeometryCone3D, weighted: b
     return out
 
 
-def fp_adjoint_tensor(sino: torch.Tensor, geom, step: float) -> torch.Tensor:
-    """Exact transpose A^T of the ray-driven forward projector (matched adjoint)."""
+def fp_adjoint_tensor(sino: torch.Tensor, geom, step: float, deterministic: bool | None = None) -> torch.Tensor:
+    """Exact transpose A^T of the ray-driven forward projector (matched adjoint).
+
+    The scatter sums in fp32 atomics (order-dependent rounding).  ``deterministic``
+    (default: ``torch.are_deterministic_algorithms_enabled()``) switches the cone
+    transpose to 64-bit fixed-point accumulation: bit-reproducible results."""
     sino = _prep(sino, geom.sinogram_shape, "sinogram")
+    if deterministic is None:
+        deterministic = torch.are_deterministic_algorithms_enabled()
     with torch.cuda.device(sino.device):
         s = _lib.stream_ptr(sino.device)
         out = _new(geom.volume_shape, sino)
@@ -245,8 +251,9 @@ def fp_adjoint_tensor(sino: torch.Tensor, geom, step: float) -> torch.Tensor:
             nz, ny, nx = geom.volume_shape
             sz, sy, sx = geom.volume_spacing
             rows, cols = geom.detector_shape
-            _lib.call("tk_forward_cone_3d_adjoint", _lib.dev_ptr(sino), geom.n_projections, rows,
-                      cols, psrc, pminv, nz, ny, nx, sz, sy, sx, float(step), _lib.dev_ptr(out), s)
+            _lib.call("tk_forward_cone_3d_adjoint_ex", _lib.dev_ptr(sino), geom.n_projections, rows,
+                      cols, psrc, pminv, nz, ny, nx, sz, sy, sx, float(step), int(bool(deterministic)),
+                      _lib.dev_ptr(out), s)
             return out
         if isinstance(geom, GeometryParallel2D):
             (c, pc), (sn, ps) = (_lib.host_f64(a) for a in geom.trig)

@@ -60,5 +60,6 @@ for adj in ("paired", "matched"):
 res["fp_ms"] = timed(lambda: fp_tensor(x0, geom, 0.5 * vs))
 res["bp_ms"] = timed(lambda: bp_tensor(y, geom, False))
 res["fp_adjoint_ms"] = timed(lambda: fp_adjoint_tensor(y, geom, 0.5 * vs))
+res["fp_adjoint_deterministic_ms"] = timed(lambda: fp_adjoint_tensor(y, geom, 0.5 * vs, deterministic=True))
 res["bp_adjoint_ms"] = timed(lambda: bp_adjoint_tensor(x0, geom, False))
 print(json.dumps(res))

@@ -649,3 +649,27 @@ def test_fp_fixed_row_stride_layout_matches_runtime_stride(tk, monkeypatch):
     monkeypatch.setenv("TK_FPZ_NOFIX", "1")
     b = tk.forward_project(tk.Volume(x, sp), geom).data
     assert torch.equal(a, b) and float(a.abs().max()) > 0
+
+
+def test_deterministic_cone_transpose(tk, oracle):
+    """Fixed-point A^T: matches the oracle's exact transpose, is bit-identical across
+    runs, and agrees with the fp32-atomic transpose to rounding."""
+    from paper_2511_08427_b200.projectors import fp_adjoint_tensor
+
+    shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
+    hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
+    geom = tk.GeometryCone3D(shape, sp, (30, 34), (1.5, 1.4), hel, 1200.0, 750.0)
+    y = np.random.default_rng(33).standard_normal((11, 30, 34))
+    yt = T(y)
+    a = fp_adjoint_tensor(yt, geom, 0.45, deterministic=True)
+    b = fp_adjoint_tensor(yt, geom, 0.45, deterministic=True)
+    assert torch.equal(a, b)
+    assert rel(a, oracle.forward_cone_3d_T(y, shape, sp, geom.matrix_array(), 0.45)) < TOL
+    assert rel(a, fp_adjoint_tensor(yt, geom, 0.45, deterministic=False).cpu().numpy()) < 1e-6
+    assert float(fp_adjoint_tensor(torch.zeros_like(yt), geom, 0.45, deterministic=True).abs().max()) == 0.0
+    torch.use_deterministic_algorithms(True)
+    try:
+        c = fp_adjoint_tensor(yt, geom, 0.45)  # follows torch's determinism switch
+    finally:
+        torch.use_deterministic_algorithms(False)
+    assert torch.equal(a, c)
