@@ -256,6 +256,7 @@ def fp_adjoint_tensor(sino: torch.Tensor, geom, step: float, deterministic: bool
                       _lib.dev_ptr(out), s)
             return out
         if isinstance(geom, GeometryParallel2D):
+            _alert_nondeterministic("the 2D forward-projection transpose")
             (c, pc), (sn, ps) = (_lib.host_f64(a) for a in geom.trig)
             ny, nx = geom.volume_shape
             sy, sx = geom.volume_spacing
@@ -271,10 +272,26 @@ def fp_adjoint_tensor(sino: torch.Tensor, geom, step: float, deterministic: bool
     raise TypeError(f"unsupported geometry {type(geom).__name__}")
 
 
+def _alert_nondeterministic(what: str) -> None:
+    """torch's convention for an op without a deterministic implementation while
+    torch.use_deterministic_algorithms(True) is on: raise (or warn if warn_only)."""
+    if torch.are_deterministic_algorithms_enabled():
+        msg = (f"{what} sums with fp32 atomics and has no deterministic implementation; "
+               "use adjoint='paired' or disable torch.use_deterministic_algorithms")
+        if torch.is_deterministic_algorithms_warn_only_enabled():
+            import warnings
+
+            warnings.warn(msg)
+        else:
+            raise RuntimeError(msg)
+
+
 def bp_adjoint_tensor(vol: torch.Tensor, geom: GeometryCone3D, weighted: bool = False) -> torch.Tensor:
-    """Exact transpose B^T of the voxel-driven cone back projector."""
+    """Exact transpose B^T of the voxel-driven cone back projector (fp32 atomics:
+    summation order not deterministic; raises under torch deterministic mode)."""
     if not isinstance(geom, GeometryCone3D):
         raise TypeError("the exact back-projection transpose is implemented for cone geometry")
+    _alert_nondeterministic("the cone back-projection transpose")
     vol = _prep(vol, geom.volume_shape, "volume")
     with torch.cuda.device(vol.device):
         out = _new(geom.sinogram_shape, vol)

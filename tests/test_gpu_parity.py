@@ -673,3 +673,25 @@ def test_deterministic_cone_transpose(tk, oracle):
     finally:
         torch.use_deterministic_algorithms(False)
     assert torch.equal(a, c)
+
+
+def test_nondeterministic_transposes_follow_torch_determinism(tk):
+    """Under torch.use_deterministic_algorithms(True) the atomic-only transposes raise
+    (torch's convention), warn with warn_only=True, and the cone A^T switches to its
+    fixed-point form."""
+    from paper_2511_08427_b200.projectors import bp_adjoint_tensor, fp_adjoint_tensor
+
+    geom = cone(tk, 12, 10, 1.7, 5)
+    x = torch.rand(12, 12, 12, device="cuda")
+    y = torch.rand(5, 10, 10, device="cuda")
+    torch.use_deterministic_algorithms(True)
+    try:
+        with pytest.raises(RuntimeError, match="deterministic"):
+            bp_adjoint_tensor(x, geom)
+        assert torch.equal(fp_adjoint_tensor(y, geom, 0.5), fp_adjoint_tensor(y, geom, 0.5, deterministic=True))
+        torch.use_deterministic_algorithms(True, warn_only=True)
+        with pytest.warns(UserWarning):
+            bp_adjoint_tensor(x, geom)
+    finally:
+        torch.use_deterministic_algorithms(False)
+    bp_adjoint_tensor(x, geom)  # fine when the switch is off
