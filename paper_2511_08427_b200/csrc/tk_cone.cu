@@ -2260,10 +2260,11 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
     const char *nofix = getenv("TK_FPZ_NOFIX");  // 1: runtime y stride (no immediate-offset far-row loads)
     if (!plan->diff && !(nofix && atoi(nofix))) {
       // fixed y stride: z pitch == 255 (mod 256) keeps the floor bias zero
-      // (1 + zp + kFpFixS == 0 mod 256); worth it when the padding is < 2x
+      // (1 + zp + kFpFixS == 0 mod 256); the padding cells are never touched, so
+      // it is used whenever the padded allocation stays below 8 GB
       const unsigned zpf = (unsigned)(nz + m2) + (255u - (unsigned)(nz + m2) % 256u);
       const unsigned long long xz = (unsigned long long)(nx + m2) * zpf;
-      if (xz <= kFpFixS && 2 * (unsigned long long)(nx + m2) * (nz + m2) >= kFpFixS) {
+      if (xz <= kFpFixS && (unsigned long long)(ny + m2) * kFpFixS * sizeof(float4) <= (8ull << 30)) {
         plan->zpitch = zpf;
         plan->xpitch = (unsigned)(nx + m2);
         plan->ystride = kFpFixS;
