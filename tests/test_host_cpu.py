@@ -232,3 +232,19 @@ def test_tapered_pipeline_chunks_cover_views_once():
                     if n > max(1, small):
                         short = ch[0] if head else ch[-1]
                         assert short[1] - short[0] == max(1, small)
+
+
+def test_bp_tile_bank_model_supports_the_8x4_warp_and_pitch_rule():
+    """The back projector's warp footprint / tile pitch choice (tk_bp_tma.cu) rests on
+    scripts/bp_bank_model.py: at cfg4, 8 x 4 warps with a pitch == 12 or 20 (mod 32)
+    need ~1 LDS wavefront per instruction, 16 x 2 warps ~1.3."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bp_bank_model", ROOT / "scripts" / "bp_bank_model.py")
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    views = range(30, 720, 90)  # oblique and near-axis views
+    blocks = ((3, 5, 2), (16, 16, 8), (28, 9, 13))
+    assert m.model(52, 8, 4, views, blocks) < 1.05
+    assert m.model(44, 8, 4, views, blocks) < 1.05
+    assert m.model(52, 16, 2, views, blocks) > 1.25
