@@ -2358,7 +2358,7 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     const int rbz = rbe ? atoi(rbe) : 8;
     const char *vge = getenv("TK_FPZ_VG");  // consecutive views per CTA: 4 (default), 1, 2, 6, 8
     // default: 8 views per CTA for long orbits (0.7 % over 4 at cfg4), 4 for short view blocks
-    const int vgz = rbz != 8 ? 1 : (vge ? atoi(vge) : (pl.f2 && n_views >= 128 ? 8 : 4));
+    const int vgz = (rbz != 8 || pl.diff) ? 1 : (vge ? atoi(vge) : (pl.f2 && n_views >= 128 ? 8 : 4));
     const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * ceil_div(n_views, vgz);
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)

@@ -397,6 +397,15 @@ class TestProperties:
 # ---------------------------------------------------------------------------
 
 
+def _poison(shape):
+    """Leave a NaN-filled block of this size in torch's caching allocator, so an output
+    the next call allocates with torch.empty starts as NaN: a kernel that misses part
+    of its output (e.g. a grid/CTA-shape mismatch) fails loudly instead of reading
+    back a stale correct result from an earlier call."""
+    t = torch.full(shape, float("nan"), device="cuda")
+    del t
+
+
 @pytest.mark.parametrize("algo", ["ldg4m", "ldg4z", "ldg4zq", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
 def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     monkeypatch.setenv("TK_FP_ALGO", algo)
@@ -404,15 +413,26 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
                              tk.circular_trajectory_3d(17, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4)),
                              1200.0, 750.0)
     x = np.random.default_rng(21).standard_normal((24, 28, 20))
+    _poison((17, 30, 34))
     got = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), geom).data
+    assert bool(torch.isfinite(got).all())
     want = oracle.forward_cone_3d(x, (0.9, 1.1, 1.0), geom.matrix_array(), (30, 34), 0.45)
     assert rel(got, want) < TOL
     g = oracle  # helical trajectory (non-circular orbit)
     hel = tk.helical_trajectory_3d(13, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
     gh = tk.GeometryCone3D((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4), hel, 1200.0, 750.0)
+    _poison((13, 30, 34))
     got = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), gh).data
+    assert bool(torch.isfinite(got).all())
     want = g.forward_cone_3d(x, (0.9, 1.1, 1.0), gh.matrix_array(), (30, 34), 0.45)
     assert rel(got, want) < TOL
+    # a long orbit (>= 128 views: 8 views per CTA in the default kernel)
+    gl = tk.circular_cone_geometry((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4), 131, 2 * np.pi,
+                                   1200.0, 750.0)
+    _poison((131, 30, 34))
+    got = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), gl).data
+    assert bool(torch.isfinite(got).all())
+    assert rel(got, g.forward_cone_3d(x, (0.9, 1.1, 1.0), gl.matrix_array(), (30, 34), 0.45)) < TOL
 
 
 @pytest.mark.parametrize("face", ["1", "0"])
