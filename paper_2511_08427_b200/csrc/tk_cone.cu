@@ -2280,7 +2280,8 @@ static int fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, d
       TK_LAUNCHED("quad_volume_z_kernel");
     } else {  // coefficient cells (ldg4z)
       const char *f2e = getenv("TK_FPZ_F2");  // 1 (default): FFMA2 / FADD2 pair march
-      plan->f2 = plan->fixs && !(f2e && !atoi(f2e));
+      const char *rbe = getenv("TK_FPZ_RB");  // the pair (A, C, B, D) layout is read only by RB = 8 kernels
+      plan->f2 = plan->fixs && !(f2e && !atoi(f2e)) && !(rbe && atoi(rbe) != 8);
       coef_volume_z_kernel<<<tg, 256, 0, st>>>(vol, nz, ny, nx, static_cast<float4 *>(plan->qA), (int)plan->zpitch,
                                                (long long)plan->ystride, plan->f2 ? 1 : 0);
       TK_LAUNCHED("coef_volume_z_kernel");
@@ -2358,7 +2359,10 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
     const int rbz = rbe ? atoi(rbe) : 8;
     const char *vge = getenv("TK_FPZ_VG");  // consecutive views per CTA: 4 (default), 1, 2, 6, 8
     // default: 8 views per CTA for long orbits (0.7 % over 4 at cfg4), 4 for short view blocks
-    const int vgz = (rbz != 8 || pl.diff) ? 1 : (vge ? atoi(vge) : (pl.f2 && n_views >= 128 ? 8 : 4));
+    int vgz = (rbz != 8 || pl.diff) ? 1 : (vge ? atoi(vge) : (pl.f2 && n_views >= 128 ? 8 : 4));
+    // only instantiated (views-per-CTA, kernel) combinations: the grid must match the kernel's VG
+    if (pl.f2 ? !(vgz == 2 || vgz == 4 || vgz == 8) : !(vgz == 1 || vgz == 2 || vgz == 4 || vgz == 6)) vgz = 4;
+    if (rbz != 8 || pl.diff) vgz = 1;
     const long long nbz = (long long)ceil_div(cols, 128 / rbz) * ceil_div(rows, rbz) * ceil_div(n_views, vgz);
     if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kern = pl.diff ? (minb >= 12 ? cone_fp4z_kernel<12, false> : cone_fp4z_kernel<10, false>)

@@ -715,3 +715,22 @@ def test_nondeterministic_transposes_follow_torch_determinism(tk):
     finally:
         torch.use_deterministic_algorithms(False)
     bp_adjoint_tensor(x, geom)  # fine when the switch is off
+
+
+@pytest.mark.parametrize("knobs", [{"TK_FPZ_RB": "16"}, {"TK_FPZ_RB": "32"}, {"TK_FPZ_VG": "1"},
+                                   {"TK_FPZ_VG": "2"}, {"TK_FPZ_VG": "6"}, {"TK_FPZ_VG": "8"},
+                                   {"TK_FPZ_VG": "5"}, {"TK_FPZ_F2": "0"}, {"TK_FPZ_NOFIX": "1"}])
+def test_fp_tuning_knobs_keep_results(tk, monkeypatch, knobs):
+    """Every forward-projector tuning knob (CTA shape, views per CTA, pair layout,
+    fixed stride) must give the default's projection (same taps; bit-identical or
+    rounding-level), with no output element missed."""
+    geom = tk.circular_cone_geometry((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4), 131, 2 * np.pi,
+                                     1200.0, 750.0)
+    x = torch.rand(24, 28, 20, device="cuda")
+    want = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), geom).data.clone()
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    _poison((131, 30, 34))
+    got = tk.forward_project(tk.Volume(x, (0.9, 1.1, 1.0)), geom).data
+    assert bool(torch.isfinite(got).all())
+    assert rel(got, want.cpu().numpy()) < 1e-6
