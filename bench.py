@@ -2,26 +2,36 @@
 """Benchmark: cone-beam forward + FDK back-projection GUPS at 512^3 x 720 views.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+                    [--fdk zslab|angle] [--chunks C] [--dry-run]
 
 One step = forward projection A x of a 512^3 Shepp-Logan volume (0.5 mm) to a
-720-view 1024^2 (0.6 mm) circular cone-beam sinogram, then FDK
-(cosine pre-weight + shepp_logan row filter + (sid/w)^2-weighted voxel-driven
-back projection + pi/V) of that sinogram.  Both operators count N_vox * V
-voxel-view updates, so value = 2 * 512^3 * 720 / step time (whole job).
-N > 1: views sharded for A + one NCCL all-gather of the sinogram, z-slabs
-(with cropped detector row bands) for FDK -- fixed total work (strong scaling).
+720-view 1024^2 (0.6 mm) circular cone-beam sinogram, then FDK (cosine
+pre-weight + shepp_logan row filter + (sid/w)^2-weighted voxel-driven back
+projection + pi/V) of that sinogram.  Both operators count N_vox * V voxel-view
+updates, so value = 2 * 512^3 * 720 / step time (whole job, strong scaling).
 
-Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching
-stream, barrier + synchronize around the K timed steps, max over ranks.
+N > 1 (one process per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run with N ranks): views sharded for A; the FDK is
+z-slab sharded, each rank receiving only its detector row band of every view
+through an uneven NCCL all-to-all issued per view chunk under the next chunk's
+projection (`--fdk zslab`, default), or angle-sharded with a reduce-scatter of
+partial volumes (`--fdk angle`, the comparison path).
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream,
+barrier + synchronize around the K timed steps, max over ranks.
+`--impl reference` times the reference's own CPU implementation (tomokit's
+numba kernels from baseline/_ref; the float64 C port in oracle/ when that
+install is absent) on the host cores, rank 0 only.
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,9 +49,12 @@ VIEWS = 720
 SDD, SID = 1200.0, 750.0
 STEP_SCALE = 0.5
 FILTER = "shepp_logan"
+NVOX = VOL[0] * VOL[1] * VOL[2]
 WORKLOAD = ("cfg4: cone-beam circular 512^3 @0.5 mm, 720 views over 2pi, 1024^2 detector @0.6 mm, "
             "sdd 1200 / sid 750: forward projection + FDK (shepp_logan) back-projection")
 METRIC = "cone-beam back/forward-projection GUPS at 512³×720 views, 1/2/4/8 B200 vs CPU"
+FP_KERNEL = "cone_fp4z_kernel"  # the default forward projector
+BP_KERNEL = "cone_bp_tma_kernel"  # the default back projector
 
 
 def parse():
@@ -50,14 +63,34 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--fdk", choices=["zslab", "angle"], default="zslab",
+                    help="N>1 FDK decomposition: z-slabs fed by a row-band all-to-all, or angle shards "
+                         "+ reduce-scatter")
+    ap.add_argument("--chunks", type=int, default=4, help="N>1: view chunks of the FP/all-to-all pipeline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=0, help="views in the CPU sample (0 = auto)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the N ranks (gloo, no GPU work) and report what world they formed")
     return ap.parse_args()
 
 
+def config(world: int, fdk: str, chunks: int) -> dict:
+    """The workload description -- identical in both arms."""
+    if world == 1:
+        par = "single GPU"
+    elif fdk == "zslab":
+        par = (f"dp{world}: FP views/{world}; FDK z-slabs/{world} fed by an uneven NCCL all-to-all of "
+               f"detector row bands in {chunks} view chunks")
+    else:
+        par = f"dp{world}: FP views/{world}; FDK angle shards/{world} + NCCL reduce-scatter of the volume"
+    return {"workload": WORKLOAD, "volume": list(VOL), "views": VIEWS, "detector": list(DET),
+            "step_mm": STEP_SCALE * min(SPACING), "filter": FILTER, "parallelism": par,
+            "l2": "no flush: inputs larger than L2 (sinogram 3.0 GB, volume 0.54 GB vs 126 MB L2)"}
+
+
 # ---------------------------------------------------------------------------
-# helpers
+# launch helpers
 # ---------------------------------------------------------------------------
 
 
@@ -66,6 +99,47 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` without a launcher: exec torch.distributed.run
+    with N local ranks (127.0.0.1 rendezvous) on the same arguments."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def check_world(args, world: int) -> None:
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+
+
+def run_dry(args) -> int:
+    """Form the N-rank group exactly as the real run does (gloo instead of NCCL,
+    no device work) and report it: the CPU test of the launch path."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = dist_env()
+    check_world(args, world)
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        got = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(got, t)
+        ranks = [int(x) for x in got]
+        dist.destroy_process_group()
+    else:
+        ranks = [0]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks,
+                          "config": config(world, args.fdk, args.chunks)}), flush=True)
+    return 0
 
 
 class ClockSampler:
@@ -77,7 +151,6 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.proc = None
-        self.gpu = gpu_index
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -116,60 +189,52 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def measured_peaks():
+# ---------------------------------------------------------------------------
+# roofline inputs
+# ---------------------------------------------------------------------------
+
+
+def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        if d.get("hbm_gbs"):
+            return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    return 6650.0, "fallback B200_PROFILING.md HBM copy figure"
 
 
-FP_KERNEL = "cone_fp4z_kernel"  # the default forward projector (TK_FP_ALGO=ldg4z)
-BP_KERNEL = "cone_bp_tma_kernel"  # the default back projector (TK_BP_ALGO=tma)
+def l1_peak():
+    """The L1 load-path ceiling measured NOW, on this lease (libtkprobe.so:
+    LDG.128 with every quarter-warp on one L1-resident line, and conflict-free
+    LDS.32).  Falls back to the newest committed probe JSON."""
+    try:
+        lib = ctypes.CDLL(str(ROOT / "paper_2511_08427_b200" / "libtkprobe.so"))
+        out = (ctypes.c_double * 4)()
+        if lib.tkp_l1_peak(out) == 0 and out[0] > 0:
+            return {"ldg128_gbs": round(out[0], 1), "lds32_gbs": round(out[1], 1), "sms": int(out[2]),
+                    "max_clock_mhz": out[3], "source": "measured on this lease (libtkprobe.so tkp_l1_peak)"}
+    except OSError:
+        pass
+    probes = sorted((ROOT / "profiles").glob("l1_peak_*.json"), reverse=True)
+    if probes:
+        d = json.loads(probes[0].read_text())
+        d["source"] = f"profiles/{probes[0].name} (committed probe, earlier lease)"
+        return d
+    return {"ldg128_gbs": 36380.0, "lds32_gbs": 30900.0, "source": "round-1 probe values"}
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the newest committed
-    ncu capture of the same configuration (profiles/ncu_*.json)."""
-    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), reverse=True):  # newest round/letter first
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest committed full ncu
+    capture of the cfg4 configuration (profiles/ncu_*.json)."""
+    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
         except (ValueError, OSError):
             continue
-        k = d.get(FP_KERNEL) or {}
+        k = d.get(kernel) or {}
         if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
             return float(k["dram_bytes_per_launch"]), f"profiles/{p.name}"
     return None, None
-
-
-def gather_roofline(fp_bytes, fp_ms, bp_bytes, bp_ms, clocks):
-    """Both projectors are gather-bound: their ceiling is the L1 load data path
-    (LSU writeback, 128 B/clk/SM; ncu derived__l1tex__lsu_writeback_bytes
-    peak_sustained = 128 x 148 B/cycle), not HBM.  Algorithmic bytes: 32 B per
-    trilinear sample (FP), 16 B per bilinear update (BP), SURVEY 8(d)."""
-    p = ROOT / "MEASURED_PEAKS.json"
-    sms = 148
-    mhz = (clocks or {}).get("sm_mhz")
-    if not mhz and p.exists():
-        mhz = json.loads(p.read_text()).get("sm_max_mhz")
-    mhz = float(mhz or 1965.0)
-    per_clk, src = 128.0, "nominal 128 B/clk/SM"
-    probes = sorted((ROOT / "profiles").glob("l1_peak_*.json"), reverse=True)  # scripts/l1_peak.cu
-    if probes:
-        try:
-            per_clk = float(json.loads(probes[0].read_text())["ldg128_bytes_per_clk_sm"])
-            src = f"measured LDG.128 {per_clk:.1f} B/clk/SM (profiles/{probes[0].name}, scripts/l1_peak.cu)"
-        except (ValueError, KeyError, OSError):
-            pass
-    peak = per_clk * sms * mhz * 1e6 / 1e9  # GB/s
-    fp = fp_bytes / (fp_ms * 1e-3) / 1e9
-    bp = bp_bytes / (bp_ms * 1e-3) / 1e9
-    return {"bound": "l1_load_path", "unit": "GB/s", "peak": round(peak, 1),
-            "peak_source": f"{src} x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)",
-            "forward": {"kernel": FP_KERNEL, "achieved": round(fp, 1), "frac": round(fp / peak, 4),
-                        "bytes_per_unit": "32 B per trilinear sample"},
-            "back": {"kernel": BP_KERNEL, "achieved": round(bp, 1), "frac": round(bp / peak, 4),
-                     "bytes_per_unit": "16 B per voxel-view update"}}
 
 
 def count_samples(geom, step, torch):
@@ -208,75 +273,159 @@ def count_samples(geom, step, torch):
     return total
 
 
+def roofline(samples, fp_ms, fp_views, bp_updates, bp_ms, l1):
+    """Roofline of the dominant kernel (the forward projector) against the bound
+    that binds it -- the L1 load path -- plus its HBM position.
+
+    * achieved = ALGORITHMIC gather bytes (32 B per trilinear sample x the exact
+      sample count) / CUDA-event kernel time; peak = the LDG.128
+      ceiling measured on this lease;
+    * hbm: algorithmic HBM bytes of one launch (volume read + sinogram write,
+      4 (N_vox + V R C)) against the driver-measured copy bandwidth, and the
+      ncu DRAM bytes of the same kernel over those algorithmic bytes (re-reads).
+    """
+    peak = float(l1["ldg128_gbs"])
+    fp_bytes = 32.0 * samples
+    achieved = fp_bytes / (fp_ms * 1e-3) / 1e9
+    hbm, hbm_src = hbm_peak()
+    alg_hbm = 4.0 * (NVOX + fp_views * DET[0] * DET[1])
+    traffic, traffic_src = ncu_traffic(FP_KERNEL)
+    bp_ach = 16.0 * bp_updates / (bp_ms * 1e-3) / 1e9
+    bp_traffic, bp_src = ncu_traffic(BP_KERNEL)
+    return {
+        "bound": "l1_load_path", "kernel": FP_KERNEL, "achieved": round(achieved, 1), "peak": round(peak, 1),
+        "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+        "algorithmic_bytes_per_launch": fp_bytes,
+        "peak_source": f"LDG.128 L1 ceiling, {l1.get('source')}",
+        "traffic_source": traffic_src,
+        "hbm": {"algorithmic_bytes_per_launch": alg_hbm, "achieved": round(alg_hbm / (fp_ms * 1e-3) / 1e9, 1),
+                "peak": hbm, "frac": round(alg_hbm / (fp_ms * 1e-3) / 1e9 / hbm, 5), "peak_source": hbm_src,
+                "traffic_over_algorithmic": round(traffic / alg_hbm, 2) if traffic else None},
+        "back": {"kernel": BP_KERNEL, "bound": "l1_load_path", "achieved": round(bp_ach, 1),
+                 "peak": round(peak, 1), "frac": round(bp_ach / peak, 4),
+                 "lds32_peak": l1.get("lds32_gbs"),
+                 "frac_of_lds32": round(bp_ach / float(l1["lds32_gbs"]), 4) if l1.get("lds32_gbs") else None,
+                 "bytes_per_unit": "16 B per voxel-view update", "traffic": bp_traffic,
+                 "traffic_source": bp_src},
+    }
+
+
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle: float64 C restatement of the reference kernels)
+# CPU arms: the reference's own numba kernels (baseline/_ref) or the C port
 # ---------------------------------------------------------------------------
 
 
-def cpu_sample(n_views: int):
-    """Time the oracle on `n_views` views spread over the 720-view orbit at full
-    resolution; returns (gups_combined, fp_gups, fdk_gups, threads, seconds, desc)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def _tomokit():
+    """Import the unmodified reference (tomokit) from baseline/_ref, numba on every host thread."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tomokit").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tk_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import numba
+
+        import tomokit  # noqa: F401
+        from tomokit import _kernels
+    except ImportError:
+        return None
+    numba.set_num_threads(os.cpu_count() or 1)
+    _kernels.warmup()  # compile once (pkg/tests/conftest.py:11-15)
+    return numba.get_num_threads()
+
+
+def sample_views(n_views: int):
     import numpy as np
 
-    import oracle as ora
-
-    threads = ora.num_threads()
-    mats_all = ora.circular_matrices(VIEWS, 2 * math.pi, SDD, SID, DET, DET_SP)
-    idx = np.linspace(0, VIEWS, n_views, endpoint=False).astype(int)
-    mats = mats_all[idx]
-    vol = ora.shepp_logan_3d(VOL)
-    step = ora.step_of(SPACING, STEP_SCALE)
-    t0 = time.perf_counter()
-    sino = ora.forward_cone_3d(vol, SPACING, mats, DET, step)
-    t1 = time.perf_counter()
-    filt = ora.filter_stage_cone(sino, SDD, SID, DET_SP, FILTER)
-    rec = ora.back_cone_3d(filt, mats, SID, VOL, SPACING, weighted=True)
-    rec *= math.pi / VIEWS
-    t2 = time.perf_counter()
-    nvox = VOL[0] * VOL[1] * VOL[2]
-    fp_gups = nvox * n_views / (t1 - t0) / 1e9
-    fdk_gups = nvox * n_views / (t2 - t1) / 1e9
-    comb = 2 * nvox * n_views / (t2 - t0) / 1e9
-    desc = (f"oracle (float64 C + OpenMP, bit-exact to the reference kernels) on {n_views} of 720 "
-            f"views spread over the orbit, full 512^3 / 1024^2 resolution; FP {t1 - t0:.2f} s, "
-            f"filter+BP {t2 - t1:.2f} s; GUPS extrapolate linearly in views")
-    return comb, fp_gups, fdk_gups, threads, t2 - t0, desc
+    return np.linspace(0, VIEWS, n_views, endpoint=False).astype(int)
 
 
-def auto_cpu_views(threads: int) -> int:
-    # ~0.8 s per view of FP + ~0.2 s of FDK on 8 cores: aim for ~10-30 s of CPU work
-    return int(min(48, max(4, threads // 2)))
+class CpuArm:
+    """One bounded sample of the workload on the host: the full 512^3 volume and
+    1024^2 detector on `n_views` views spread over the 720-view orbit, forward
+    projection + FDK.  GUPS is a rate, so the sample's rate is the value."""
+
+    def __init__(self, n_views: int):
+        self.n_views = n_views
+        self.threads = _tomokit()
+        self.kind = "reference" if self.threads else "port"
+        if self.kind == "reference":
+            from tomokit import filters, geometry, phantoms, projectors
+
+            mats = geometry.circular_trajectory_3d(VIEWS, 2 * math.pi, SDD, SID, DET, DET_SP)
+            self.geom = geometry.GeometryCone3D(VOL, SPACING, DET, DET_SP,
+                                                [mats[i] for i in sample_views(n_views)], SDD, SID)
+            self.vol = phantoms.shepp_logan_3d(VOL, SPACING)
+            self._fp = lambda: projectors.forward_project_cone_3d(self.vol, self.geom)
+            self._fdk = lambda s: filters.fdk_cone_3d(s, self.geom, FILTER)
+        else:
+            sys.path.insert(0, str(ROOT / "oracle"))
+            import oracle as ora
+
+            self.threads = ora.num_threads()
+            mats = ora.circular_matrices(VIEWS, 2 * math.pi, SDD, SID, DET, DET_SP)[sample_views(n_views)]
+            vol = ora.shepp_logan_3d(VOL)
+            step = ora.step_of(SPACING, STEP_SCALE)
+            self._fp = lambda: ora.forward_cone_3d(vol, SPACING, mats, DET, step)
+            self._fdk = lambda s: ora.fdk_cone_3d(s, mats, SDD, SID, DET_SP, VOL, SPACING, FILTER)
+
+    def describe(self) -> str:
+        what = ("tomokit (the unmodified reference, baseline/_ref) numba kernels, "
+                "forward_project_cone_3d + fdk_cone_3d" if self.kind == "reference"
+                else "oracle/ float64 C + OpenMP port of the reference kernels (tomokit not importable)")
+        return (f"{what} on {self.threads} threads ({cpu_model()}); sample = {self.n_views} of 720 views "
+                f"spread over the orbit at the full 512^3 volume / 1024^2 detector")
+
+    def run(self):
+        t0 = time.perf_counter()
+        sino = self._fp()
+        t1 = time.perf_counter()
+        self._fdk(sino)
+        t2 = time.perf_counter()
+        upd = NVOX * self.n_views
+        return {"gups": 2 * upd / (t2 - t0) / 1e9, "fp_gups": upd / (t1 - t0) / 1e9,
+                "fdk_gups": upd / (t2 - t1) / 1e9, "seconds": t2 - t0, "fp_s": t1 - t0, "fdk_s": t2 - t1}
+
+
+def default_cpu_views() -> int:
+    return 8  # ~4-8 s per FP+FDK sample on 16 host cores
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle as ora
-
-    threads = ora.num_threads()
-    nv = args.cpu_views or auto_cpu_views(threads)
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(max(1, nv // 4))
-    vals, secs = [], 0.0
-    desc = ""
-    for _ in range(args.steps):
-        comb, fpg, fdkg, threads, sec, desc = cpu_sample(nv)
-        vals.append(comb)
-        secs += sec
-    value = statistics.median(vals)
-    ms_step = 2 * VOL[0] * VOL[1] * VOL[2] * VIEWS / (value * 1e9) * 1e3
+    arm = CpuArm(args.cpu_views or default_cpu_views())  # compiles the numba kernels (warmup())
+    for _ in range(args.warmup):
+        arm.run()  # untimed
+    runs = [arm.run() for _ in range(args.steps)]
+    secs = sum(r["seconds"] for r in runs)
+    value = 2 * NVOX * arm.n_views * len(runs) / secs / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GUPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms_step, 1), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": round(secs / len(runs) * 1e3, 1), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic Shepp-Logan 512^3 phantom",
-        "config": {"workload": WORKLOAD, "sample_views": nv},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GUPS", "cores": threads, "kind": "port",
-                         "sample": desc},
+        "config": config(args.gpus, args.fdk, args.chunks),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GUPS", "cores": arm.threads, "kind": arm.kind,
+                         "cpu_model": cpu_model(), "sample": arm.describe(),
+                         "fp_gups": round(statistics.median(r["fp_gups"] for r in runs), 4),
+                         "fdk_gups": round(statistics.median(r["fdk_gups"] for r in runs), 4)},
         "e2e": {"value": round(value, 4), "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "each step is one bounded sample (the sample's views at full resolution); ms_per_step is "
+                "that sample's time, value its GUPS rate",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -298,11 +447,12 @@ def run_ours(args):
     from paper_2511_08427_b200.projectors import bp_cone_tensor_ex, fp_tensor
 
     world, rank, local = dist_env()
+    check_world(args, world)
     # TK_BENCH_BACKEND=gloo runs the multi-rank code path with several ranks
     # sharing the visible GPU(s) -- a functional check of the sharding, row bands
     # and collectives on a 1-GPU box, not a measurement (the driver uses NCCL)
-    backend = os.environ.get("TK_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
+    backend = os.environ.get("TK_BENCH_BACKEND", "nccl") if world > 1 else "none"
+    if backend == "gloo":
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -312,38 +462,63 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     _lib.load()
+    l1 = l1_peak() if rank == 0 else None
 
     geom = tk.circular_cone_geometry(VOL, SPACING, DET, DET_SP, VIEWS, 2 * math.pi, SDD, SID)
     step = STEP_SCALE * min(SPACING)
     vb, ve = D.shard_bounds(VIEWS, world, rank)
     sub = D.subset_geometry(geom, slice(vb, ve))
-    z0, z1 = D.shard_bounds(VOL[0], world, rank)
-    r0, r1 = D.row_band(geom, z0, z1) if world > 1 else (0, DET[0])
-    counts = [D.shard_bounds(VIEWS, world, r)[1] - D.shard_bounds(VIEWS, world, r)[0] for r in range(world)]
+    bands = D.slab_bands(geom, world)
+    z0, z1, r0, r1 = bands[rank]
+    angle = world > 1 and args.fdk == "angle"
+    if angle:
+        z0, z1 = rank * VOL[0] // world, (rank + 1) * VOL[0] // world
+    n_chunks = max(1, args.chunks) if world > 1 else 1
 
     vol = tk.phantoms.shepp_logan_3d(VOL, device=dev)
-    local_sino = torch.empty((ve - vb, *DET), dtype=torch.float32, device=dev)
-    band = torch.empty((VIEWS, r1 - r0, DET[1]), dtype=torch.float32, device=dev)
-    slab = torch.empty((z1 - z0, VOL[1], VOL[2]), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    if world == 1:
+        sino = torch.empty((VIEWS, *DET), dtype=torch.float32, device=dev)
+        filt = torch.empty_like(sino)
+        slab = torch.empty(VOL, dtype=torch.float32, device=dev)
+    elif angle:
+        sino = torch.empty((ve - vb, *DET), dtype=torch.float32, device=dev)
+        filt = torch.empty_like(sino)
+    else:
+        band_raw = torch.empty((VIEWS, r1 - r0, DET[1]), dtype=torch.float32, device=dev)
+        band = torch.empty_like(band_raw)
+        slab = torch.empty((z1 - z0, VOL[1], VOL[2]), dtype=torch.float32, device=dev)
+    order = None
 
     def step_fn(ev=None):
-        if ev:
-            ev[0].record(stream)
-        fp_tensor(vol, sub, step, out=local_sino)
-        if ev:
-            ev[1].record(stream)
-        full = D.gather_views(local_sino, counts) if world > 1 else local_sino
-        if ev:
-            ev[2].record(stream)
-        src = full[:, r0:r1, :].contiguous() if world > 1 else full
-        filter_stage_tensor(src, geom, FILTER, out=band, row_offset=r0)
-        if ev:
-            ev[3].record(stream)
-        bp_cone_tensor_ex(band, geom, True, r0, z0, z1 - z0, out=slab)
-        slab.mul_(math.pi / VIEWS)
-        if ev:
-            ev[4].record(stream)
+        nonlocal order, slab
+        rec = (lambda i: ev[i].record(stream)) if ev else (lambda i: None)
+        rec(0)
+        if world == 1:
+            fp_tensor(vol, geom, step, out=sino)
+            rec(1)
+            rec(2)
+            filter_stage_tensor(sino, geom, FILTER, out=filt)
+            rec(3)
+            bp_cone_tensor_ex(filt, geom, True, 0, 0, VOL[0], out=slab)
+            slab.mul_(math.pi / VIEWS)
+        elif angle:
+            fp_tensor(vol, sub, step, out=sino)
+            rec(1)
+            rec(2)
+            filter_stage_tensor(sino, geom, FILTER, out=filt)
+            rec(3)
+            _, slab = D.fdk_angle_sharded(filt, geom, FILTER, rank, world, filter_fn=lambda s: s)
+        else:
+            _, order = D.forward_project_and_exchange(
+                vol, geom, step, rank, world, n_chunks=n_chunks, bands=bands, out=band_raw,
+                on_chunk=lambda k: rec(1) if k == n_chunks - 1 else None)
+            rec(2)  # the stream has waited for every chunk's all-to-all
+            filter_stage_tensor(band_raw, geom, FILTER, out=band, row_offset=r0)
+            rec(3)
+            bp_cone_tensor_ex(band, geom, True, r0, z0, z1 - z0, out=slab, views=order)
+            slab.mul_(math.pi / VIEWS)
+        rec(4)
 
     for _ in range(args.warmup):
         step_fn()
@@ -373,64 +548,51 @@ def run_ours(args):
     t = torch.tensor([elapsed, *ph], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed, fp_ms, gather_ms, filt_ms, bp_ms = (float(v) for v in t.cpu())
+    elapsed, fp_ms, xchg_ms, filt_ms, bp_ms = (float(v) for v in t.cpu())
     ms_step = elapsed / args.steps
-    nvox = VOL[0] * VOL[1] * VOL[2]
-    value = 2 * nvox * VIEWS / (ms_step * 1e-3) / 1e9
+    value = 2 * NVOX * VIEWS / (ms_step * 1e-3) / 1e9
 
-    # -- end to end through the public boundary with pinned host buffers --------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, counts, sub,
-                      z0, z1, r0, r1)
+        e2e = run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, sub, bands, n_chunks)
 
-    # -- roofline of the dominant kernel (forward projection) --------------------------
     samples = count_samples(sub, step, torch)
-    fp_bytes = 32.0 * samples  # 8 fp32 taps per trilinear sample
-    hbm_peak, peak_kind = measured_peaks()
-    achieved = fp_bytes / (fp_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic()
-    bp_updates = (z1 - z0) * VOL[1] * VOL[2] * VIEWS
+    bp_views = VIEWS if not angle else ve - vb
+    bp_updates = (z1 - z0 if not angle else VOL[0]) * VOL[1] * VOL[2] * bp_views
+    cfg = config(world, args.fdk, n_chunks)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: Shepp-Logan 512^3 phantom generated on device; 720-view circular orbit",
-        "config": {"workload": WORKLOAD, "volume": list(VOL), "views": VIEWS, "detector": list(DET),
-                   "step_mm": step, "filter": FILTER,
-                   "parallelism": f"FP views/{world} + NCCL all-gather, FDK z-slab/{world} with row bands"
-                   if world > 1 else "single GPU",
-                   "l2": "no flush: inputs larger than L2 (sinogram 3.0 GB, volume 0.54 GB vs 126 MB L2)"},
+        "config": cfg,
         "kernels": {
-            "forward_projection": {"ms": round(fp_ms, 3), "gups": round(nvox * (ve - vb) / (fp_ms * 1e-3) / 1e9, 2),
+            "forward_projection": {"ms": round(fp_ms, 3), "views": ve - vb,
+                                   "gups": round(NVOX * (ve - vb) / (fp_ms * 1e-3) / 1e9, 2),
                                    "samples": samples, "gsamples_per_s": round(samples / (fp_ms * 1e-3) / 1e9, 2)},
-            "all_gather": {"ms": round(gather_ms, 3)},
+            "exchange": {"ms": round(xchg_ms, 3),
+                         "what": "none" if world == 1 else ("row-band all-to-all tail after the last FP chunk"
+                                                            if not angle else "none (angle shards)"),
+                         "recv_bytes_per_rank": 0 if world == 1 or angle else
+                         4 * DET[1] * VIEWS * (r1 - r0) * (world - 1) // world},
             "filter": {"ms": round(filt_ms, 3)},
             "back_projection": {"ms": round(bp_ms, 3), "gups": round(bp_updates / (bp_ms * 1e-3) / 1e9, 2),
-                                "gather_gbs": round(16.0 * bp_updates / (bp_ms * 1e-3) / 1e9, 1)},
+                                "includes": "reduce-scatter of the partial volume" if angle else "pi/V scale"},
         },
-        "roofline": {"bound": "hbm", "kernel": FP_KERNEL, "achieved": round(achieved, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
-                     "note": "achieved = algorithmic gather bytes (32 B per trilinear sample x exact sample "
-                             "count) / CUDA-event kernel time; gathers are served mostly by L1/L2, so "
-                             "frac > 1 is possible -- traffic is the DRAM bytes ncu measured"},
-        "gather_roofline": gather_roofline(fp_bytes, fp_ms, 16.0 * bp_updates, bp_ms, clocks),
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,
     }
+    if rank == 0:
+        line["roofline"] = roofline(samples, fp_ms, ve - vb, bp_updates, bp_ms, l1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sys.path.insert(0, str(ROOT / "oracle"))
-            import oracle as ora
-
-            nv = args.cpu_views or auto_cpu_views(ora.num_threads())
-            comb, fpg, fdkg, threads, sec, desc = cpu_sample(nv)
-            line["cpu_baseline"] = {"value": round(comb, 4), "unit": "GUPS", "cores": threads,
-                                    "kind": "port", "sample": desc,
-                                    "fp_gups": round(fpg, 4), "fdk_gups": round(fdkg, 4)}
+            arm = CpuArm(args.cpu_views or default_cpu_views())
+            r = arm.run()
+            line["cpu_baseline"] = {"value": round(r["gups"], 4), "unit": "GUPS", "cores": arm.threads,
+                                    "kind": arm.kind, "cpu_model": cpu_model(), "sample": arm.describe(),
+                                    "seconds": round(r["seconds"], 2), "fp_gups": round(r["fp_gups"], 4),
+                                    "fdk_gups": round(r["fdk_gups"], 4)}
         except Exception as exc:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:
@@ -441,13 +603,13 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, counts, sub, z0, z1, r0, r1):
+def run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, sub, bands, n_chunks):
     """Same step through the public API with host buffers: pinned volume in,
-    H2D, forward projection, (N>1: NCCL all-gather), FDK, D2H of the
+    H2D, forward projection, (N>1: row-band exchange), FDK, D2H of the
     sinogram and of the reconstruction, every step."""
     from paper_2511_08427_b200 import ops
     from paper_2511_08427_b200.filters import filter_stage_tensor
-    from paper_2511_08427_b200.projectors import bp_cone_tensor_ex, fp_tensor
+    from paper_2511_08427_b200.projectors import bp_cone_tensor_ex
 
     host_vol = torch.empty(VOL, dtype=torch.float32, pin_memory=True)
     host_vol.copy_(vol)
@@ -462,20 +624,21 @@ def run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, counts,
             rec_h = ops.py_fbp(sino_h, cfg)                       # H2D sinogram, D2H volume
             return nbytes(host_vol) + nbytes(sino_h), nbytes(sino_h) + nbytes(rec_h)
     else:
-        host_sino = torch.empty((counts[rank], *DET), dtype=torch.float32, pin_memory=True)
+        z0, z1, r0, r1 = bands[rank]
+        host_band = torch.empty((VIEWS, r1 - r0, DET[1]), dtype=torch.float32, pin_memory=True)
         host_slab = torch.empty((z1 - z0, VOL[1], VOL[2]), dtype=torch.float32, pin_memory=True)
 
         def one():
             v = host_vol.to(dev, non_blocking=True)
-            loc = fp_tensor(v, sub, step)
-            host_sino.copy_(loc, non_blocking=True)
-            full = D.gather_views(loc, counts)
-            band = filter_stage_tensor(full[:, r0:r1, :].contiguous(), geom, FILTER, row_offset=r0)
-            sl = bp_cone_tensor_ex(band, geom, True, r0, z0, z1 - z0)
+            band, order = D.forward_project_and_exchange(v, geom, step, rank, world, n_chunks=n_chunks,
+                                                         bands=bands)
+            host_band.copy_(band, non_blocking=True)
+            f = filter_stage_tensor(band, geom, FILTER, row_offset=r0)
+            sl = bp_cone_tensor_ex(f, geom, True, r0, z0, z1 - z0, views=order)
             sl.mul_(math.pi / VIEWS)
             host_slab.copy_(sl, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
-            return nbytes(host_vol), nbytes(host_sino) + nbytes(host_slab)
+            return nbytes(host_vol), nbytes(host_band) + nbytes(host_slab)
 
     one()
     torch.cuda.synchronize()
@@ -492,15 +655,24 @@ def run_e2e(args, tk, torch, dist, D, geom, world, rank, dev, vol, step, counts,
         dist.barrier()
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     sec = float(dt.item()) / steps
-    nvox = VOL[0] * VOL[1] * VOL[2]
-    return {"value": round(2 * nvox * VIEWS / sec / 1e9, 3), "unit": "GUPS", "ms_per_step": round(sec * 1e3, 1),
+    return {"value": round(2 * NVOX * VIEWS / sec / 1e9, 3), "unit": "GUPS", "ms_per_step": round(sec * 1e3, 1),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "path": "ops.py_forward_project + ops.py_fbp on pinned host tensors" if world == 1
-            else "pinned H2D + view-sharded FP + NCCL all-gather + z-slab FDK + pinned D2H"}
+            else "pinned H2D + view-sharded FP + row-band all-to-all + z-slab FDK + pinned D2H of the "
+                 "rank's band and slab"}
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)  # does not return
+    # NCCL's communicator-init lines (ranks, NVLink/NVLS transport) go to stderr,
+    # keeping stdout for the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

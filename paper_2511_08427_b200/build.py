@@ -19,6 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtkb200.so"
+PROBE = PKG / "libtkprobe.so"  # measurement probes for bench.py (not part of the operator library)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -34,10 +35,10 @@ def sources() -> list[Path]:
 
 
 def is_stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not PROBE.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = sources() + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tk_b200.h"]
+    deps = sources() + list(CSRC.glob("*.cuh")) + list(CSRC.glob("probe/*.cu")) + [ROOT / "include" / "tk_b200.h"]
     return any(p.stat().st_mtime > t for p in deps)
 
 
@@ -71,7 +72,18 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     link = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     subprocess.run(link, check=True)
     os.replace(tmp, LIB)
+    build_probe()
     return LIB
+
+
+def build_probe() -> Path:
+    """libtkprobe.so: the L1 load-path ceiling probe bench.py runs on its own lease."""
+    tmp = PROBE.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-cudart", "static", "-o", str(tmp), str(CSRC / "probe" / "tk_probe.cu")]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, PROBE)
+    return PROBE
 
 
 if __name__ == "__main__":

@@ -1,12 +1,14 @@
-// l1_peak.cu -- measured L1 load-path ceilings on the B200 (the roofline the
-// gather kernels are reported against):
+// tk_probe.cu -- measured L1 load-path ceilings of the GPU the bench runs on
+// (the roofline the gather kernels are reported against).  Built
+// as its own library (libtkprobe.so), not part of the operator library:
 //   ldg128: every quarter-warp reads one full 128-byte line per LDG.128 from an
 //           L1-resident 32 KB buffer (best case for a vector gather);
 //   lds32:  conflict-free LDS.32, one 128-byte wavefront per warp instruction.
-// Build + run:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/l1_peak scripts/l1_peak.cu && /tmp/l1_peak
-// Prints one JSON line (bytes moved to registers per second, whole GPU).
-#include <cstdio>
+// bench.py calls tkp_l1_peak() on the same lease right before its timed
+// region; `python -m paper_2511_08427_b200.build` builds it next to libtkb200.so.
 #include <cuda_runtime.h>
+
+namespace {
 
 constexpr int kIters = 4096;
 
@@ -41,43 +43,52 @@ __global__ void __launch_bounds__(256) lds32_kernel(float *out) {
   if (acc == 1234.5f) out[threadIdx.x] = acc;
 }
 
-int main() {
+}  // namespace
+
+extern "C" {
+
+// out[0] = LDG.128 GB/s, out[1] = LDS.32 GB/s, out[2] = SM count,
+// out[3] = max SM clock (MHz, device attribute).  Returns a cudaError_t.
+int tkp_l1_peak(double *out) {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);  // kHz (max boost)
-  float4 *buf;
-  float *out;
-  cudaMalloc(&buf, 2048 * sizeof(float4));
+  float4 *buf = nullptr;
+  float *o = nullptr;
+  if (cudaMalloc(&buf, 2048 * sizeof(float4)) != cudaSuccess) return (int)cudaGetLastError();
   cudaMemset(buf, 0, 2048 * sizeof(float4));
-  cudaMalloc(&out, 1024 * sizeof(float));
+  cudaMalloc(&o, 1024 * sizeof(float));
   const int blocks = sms * 8;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float best_ldg = 1e30f, best_lds = 1e30f;
-  for (int rep = 0; rep < 5; ++rep) {
+  for (int rep = 0; rep < 6; ++rep) {
+    float ms;
     cudaEventRecord(a);
-    ldg128_kernel<<<blocks, 256>>>(buf, out, 2047u);
+    ldg128_kernel<<<blocks, 256>>>(buf, o, 2047u);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
-    float ms;
     cudaEventElapsedTime(&ms, a, b);
     if (rep) best_ldg = ms < best_ldg ? ms : best_ldg;
     cudaEventRecord(a);
-    lds32_kernel<<<blocks, 256>>>(out);
+    lds32_kernel<<<blocks, 256>>>(o);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     if (rep) best_lds = ms < best_lds ? ms : best_lds;
   }
   const double ldg_bytes = (double)blocks * 256 * kIters * 16, lds_bytes = (double)blocks * 256 * kIters * 4;
-  const double ldg_gbs = ldg_bytes / (best_ldg * 1e-3) / 1e9, lds_gbs = lds_bytes / (best_lds * 1e-3) / 1e9;
-  const double nominal = 128.0 * sms * clk * 1e3 / 1e9;
-  printf("{\"ldg128_gbs\": %.1f, \"lds32_gbs\": %.1f, \"nominal_128B_per_clk_gbs\": %.1f, \"sms\": %d, "
-         "\"max_clock_mhz\": %.0f, \"ldg128_bytes_per_clk_sm\": %.1f, \"lds32_bytes_per_clk_sm\": %.1f, "
-         "\"err\": \"%s\"}\n",
-         ldg_gbs, lds_gbs, nominal, sms, clk / 1e3, ldg_gbs * 1e9 / (sms * clk * 1e3),
-         lds_gbs * 1e9 / (sms * clk * 1e3), cudaGetErrorString(cudaGetLastError()));
-  return 0;
+  out[0] = ldg_bytes / (best_ldg * 1e-3) / 1e9;
+  out[1] = lds_bytes / (best_lds * 1e-3) / 1e9;
+  out[2] = sms;
+  out[3] = clk / 1e3;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(o);
+  return (int)cudaGetLastError();
 }
+
+}  // extern "C"

@@ -2406,6 +2406,10 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
 static int launch_fp4(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                       const double *sources, const double *minv, int n_views, int rows, int cols,
                       double step, float *out, cudaStream_t st) {
+  const char *me = getenv("TK_FP_MIRROR");  // 0: never use the z-mirror-pair kernel
+  if (fp_algo() == FpAlgo::kLdg4z && !(me && !atoi(me)) && fp_mirror_fits(nz, ny, nx) &&
+      views_z_mirror(sources, minv, n_views, rows))
+    return launch_fp_mirror(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   FpPlan plan;
   int rc = fp_plan_create(vol, nz, ny, nx, sz, sy, sx, &plan, st);
   if (rc == TK_OK) rc = fp_plan_project(plan, sources, minv, n_views, rows, cols, step, out, st);

@@ -4,7 +4,12 @@ Work is split only where it splits naturally (no reference counterpart; the
 reference is single-process):
 
 * forward projection -- contiguous view blocks per rank, volume replicated,
-  no communication until one all-gather of the sinogram (NCCL over NVLink);
+  no communication until the sinogram is exchanged (NCCL over NVLink): either
+  one all-gather of the whole sinogram (`gather_views`), or -- what the FDK
+  needs -- an uneven all-to-all that sends every rank only the detector row
+  band of each view its z-slab projects into (`exchange_row_bands`), issued
+  per view chunk so chunk k travels while chunk k+1 is projected
+  (`forward_project_and_exchange`);
 * FDK back projection -- z-slabs per rank; each rank filters and back-projects
   only the detector row band its slab projects into (band from the slab's
   corner projections through every P), so output slabs are disjoint and need
@@ -35,6 +40,12 @@ __all__ = [
     "fdk_zslab",
     "back_project_angle_sharded",
     "subset_geometry",
+    "slab_bands",
+    "chunk_bounds",
+    "received_view_order",
+    "exchange_row_bands",
+    "forward_project_and_exchange",
+    "fdk_angle_sharded",
 ]
 
 
@@ -170,3 +181,154 @@ def back_project_angle_sharded(sino_local: torch.Tensor, geom: GeometryCone3D, w
         dist.all_reduce(part, group=group)
         out.copy_(part[rank * (nz // world):(rank + 1) * (nz // world)])
     return out
+
+
+# ---------------------------------------------------------------------------
+# Row-band all-to-all (z-slab FDK fed by a view-sharded FP)
+# ---------------------------------------------------------------------------
+
+
+def slab_bands(geom: GeometryCone3D, world: int) -> list[tuple[int, int, int, int]]:
+    """(z_begin, z_end, row_begin, row_end) of every rank's z-slab and detector row band."""
+    out = []
+    for r in range(world):
+        z0, z1 = shard_bounds(geom.volume_shape[0], world, r)
+        r0, r1 = row_band(geom, z0, z1) if world > 1 else (0, geom.detector_shape[0])
+        out.append((z0, z1, r0, r1))
+    return out
+
+
+def chunk_bounds(n_views: int, n_chunks: int) -> list[tuple[int, int]]:
+    """Local [begin, end) view offsets of each pipeline chunk (balanced, possibly empty)."""
+    return [shard_bounds(n_views, n_chunks, k) for k in range(n_chunks)]
+
+
+def received_view_order(n_views: int, world: int, n_chunks: int) -> np.ndarray:
+    """Global view index of every view in the received band, in arrival layout:
+    chunk-major, then source rank, then view.  The back projection takes the
+    projection matrices in this order (its sum over views is order-free up to
+    fp32 rounding), so the received band is used in place, without a reorder."""
+    order = []
+    starts = [shard_bounds(n_views, world, g)[0] for g in range(world)]
+    counts = [shard_bounds(n_views, world, g)[1] - starts[g] for g in range(world)]
+    for k in range(n_chunks):
+        for g in range(world):
+            b, e = shard_bounds(counts[g], n_chunks, k)
+            order.extend(range(starts[g] + b, starts[g] + e))
+    return np.asarray(order, dtype=np.int64)
+
+
+def _all_to_all(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group=None,
+                async_op: bool = False):
+    """all_to_all_single of 1-D tensors with uneven splits.  NCCL runs it on its
+    own stream (async_op: returns the work handle); gloo on CUDA tensors is
+    staged through host memory (functional path for the single-GPU check)."""
+    if _backend() == "gloo" and inp.is_cuda:
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(o)
+        return None
+    return dist.all_to_all_single(out, inp, out_splits, in_splits, group=group, async_op=async_op)
+
+
+def exchange_row_bands(local: torch.Tensor, counts: list[int], bands, rank: int, out: torch.Tensor,
+                       group=None, async_op: bool = False):
+    """Send rows [r0_h, r1_h) of this rank's views to every rank h; receive this
+    rank's rows from every rank into ``out`` (sum(counts), r1 - r0, cols),
+    source blocks in rank order.
+
+    ``counts[g]`` = views rank g contributes in this exchange; ``bands[h]`` =
+    (z0, z1, r0, r1) of rank h.  Bytes received per rank = 4 * cols * (r1 - r0)
+    * sum(counts) -- its own band only, instead of the whole sinogram an
+    all-gather delivers.  Returns (work or None, send buffer to keep alive).
+    """
+    v, rows, cols = local.shape
+    if v != counts[rank]:
+        raise ValueError("local view block does not match counts[rank]")
+    my_rows = bands[rank][3] - bands[rank][2]
+    if tuple(out.shape) != (sum(counts), my_rows, cols):
+        raise ValueError("receive buffer does not match the band")
+    parts = [local[:, r0:r1, :].reshape(-1) for (_, _, r0, r1) in bands]
+    send = torch.cat(parts) if parts else local.new_empty(0)
+    in_splits = [p.numel() for p in parts]
+    out_splits = [c * my_rows * cols for c in counts]
+    work = _all_to_all(out.view(-1), send, out_splits, in_splits, group=group, async_op=async_op)
+    return work, send
+
+
+def forward_project_and_exchange(vol: torch.Tensor, geom: GeometryCone3D, step: float, rank: int,
+                                 world: int, n_chunks: int = 1, fp_fn: Callable | None = None,
+                                 bands=None, out: torch.Tensor | None = None, group=None,
+                                 on_chunk: Callable | None = None):
+    """View-sharded forward projection whose output goes straight to the z-slab
+    owners: chunk k of this rank's views is projected, then its row bands are
+    sent with an asynchronous all-to-all while chunk k+1 is projected.
+
+    Returns (band, order): band (V, r1 - r0, cols) holds this rank's detector
+    rows of every view, in ``received_view_order`` layout; ``order`` are the
+    global view indices of its rows.  ``on_chunk(k)`` is called after chunk k's
+    projection is enqueued (timing hooks).
+    """
+    if fp_fn is None:
+        from .projectors import fp_tensor as fp_fn
+    nv = geom.n_projections
+    bands = bands or slab_bands(geom, world)
+    starts = [shard_bounds(nv, world, g)[0] for g in range(world)]
+    counts = [shard_bounds(nv, world, g)[1] - starts[g] for g in range(world)]
+    _, _, r0, r1 = bands[rank]
+    rows, cols = geom.detector_shape
+    if out is None:
+        out = vol.new_empty((nv, r1 - r0, cols))
+    pending, off = [], 0
+    vb = starts[rank]
+    for k in range(n_chunks):
+        ck = [shard_bounds(counts[g], n_chunks, k) for g in range(world)]
+        ccounts = [e - b for b, e in ck]
+        total = sum(ccounts)
+        if total == 0:
+            continue
+        b, e = ck[rank]
+        if e > b:
+            local = fp_fn(vol, subset_geometry(geom, slice(vb + b, vb + e)), step)
+        else:
+            local = vol.new_empty((0, rows, cols))
+        if on_chunk is not None:
+            on_chunk(k)
+        if world == 1:
+            out[off:off + total].copy_(local[:, r0:r1, :])
+        else:
+            pending.append(exchange_row_bands(local, ccounts, bands, rank, out[off:off + total],
+                                              group=group, async_op=True))
+        off += total
+    for work, _send in pending:
+        if work is not None:
+            work.wait()
+    return out, received_view_order(nv, world, n_chunks)
+
+
+def fdk_angle_sharded(sino_local: torch.Tensor, geom: GeometryCone3D, filter_kind: str, rank: int,
+                      world: int, filter_fn: Callable | None = None, bp_fn: Callable | None = None,
+                      group=None) -> tuple[int, torch.Tensor]:
+    """Comparison FDK: filter and back-project this rank's own views (full
+    detector) into a full partial volume, then reduce-scatter z-slabs.  No
+    sinogram exchange; (world - 1) / world of the volume crosses NVLink.
+    Returns (z_begin, slab) scaled by pi / V; needs nz divisible by world."""
+    from .filters import filter_stage_tensor
+    from .projectors import bp_cone_tensor_ex
+
+    nz = geom.volume_shape[0]
+    if nz % world:
+        raise ValueError("angle-sharded FDK needs nz divisible by the world size")
+    b, e = shard_bounds(geom.n_projections, world, rank)
+    filter_fn = filter_fn or (lambda s: filter_stage_tensor(s, geom, filter_kind))
+    bp_fn = bp_fn or (lambda f: bp_cone_tensor_ex(f, geom, True, 0, 0, nz, views=slice(b, e)))
+    part = bp_fn(filter_fn(sino_local))
+    if world == 1:
+        return 0, part.mul_(math.pi / geom.n_projections)
+    out = part.new_empty((nz // world, *geom.volume_shape[1:]))
+    if _backend() == "nccl":
+        dist.reduce_scatter_tensor(out, part, group=group)
+    else:
+        dist.all_reduce(part, group=group)
+        out.copy_(part[rank * (nz // world):(rank + 1) * (nz // world)])
+    return rank * (nz // world), out.mul_(math.pi / geom.n_projections)

@@ -116,3 +116,172 @@ def test_two_rank_sharded_pipeline_matches_single_process():
     # angle-sharded back projection + reduce == full back projection
     want_bp = ora.back_cone_3d(sino.astype(np.float64), mats, geom.sid, geom.volume_shape, geom.volume_spacing, True)
     assert ora.rel_l2(part, want_bp) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# row-band all-to-all (the z-slab FDK's input path) and the comparison
+# angle-sharded FDK, world size 2 (gloo) -- and 3 (uneven views / bands)
+# ---------------------------------------------------------------------------
+
+
+def _a2a_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(ROOT))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_08427_b200 import distributed as D
+
+        geom = _geom()
+        ora, fp_fn, filter_fn, bp_fn, bp_full = _oracle_fns(geom)
+        x = torch.from_numpy(np.random.default_rng(0).standard_normal(geom.volume_shape)).float()
+        bands = D.slab_bands(geom, world)
+        res = {}
+        for n_chunks in (1, 3):
+            calls = []
+            band, order = D.forward_project_and_exchange(x, geom, 0.45, rank, world, n_chunks=n_chunks,
+                                                         fp_fn=fp_fn, on_chunk=calls.append)
+            res[n_chunks] = (band.numpy(), order, len(calls))
+        # z-slab FDK straight from the received band (views in arrival order)
+        z0, z1, r0, r1 = bands[rank]
+        band, order = D.forward_project_and_exchange(x, geom, 0.45, rank, world, n_chunks=2, fp_fn=fp_fn)
+        filt = filter_fn(band, r0)
+        full = np.zeros(geom.sinogram_shape)
+        full[order, r0:r1] = filt.double().numpy()
+        slab = ora.back_cone_3d(full, geom.matrix_array(), geom.sid, geom.volume_shape,
+                                geom.volume_spacing, True)[z0:z1] * (np.pi / geom.n_projections)
+        # comparison path: angle-sharded FDK + reduce-scatter (nz = 20 splits for world 2)
+        vb, ve = D.shard_bounds(geom.n_projections, world, rank)
+        local = fp_fn(x, D.subset_geometry(geom, slice(vb, ve)), 0.45)
+
+        def bp_local(f):
+            sino = np.zeros(geom.sinogram_shape)
+            sino[vb:ve] = f.double().numpy()
+            return torch.from_numpy(ora.back_cone_3d(sino, geom.matrix_array(), geom.sid, geom.volume_shape,
+                                                     geom.volume_spacing, True)).float()
+
+        ang = None
+        if geom.volume_shape[0] % world == 0:
+            ang = D.fdk_angle_sharded(local, geom, "shepp_logan", rank, world,
+                                      filter_fn=lambda s: filter_fn(s, 0), bp_fn=bp_local)
+            ang = (ang[0], ang[1].numpy())
+        out = [None] * world
+        dist.all_gather_object(out, (rank, bands, res, (z0, slab), ang))
+        if rank == 0:
+            q.put(("ok", out))
+    except Exception as exc:  # noqa: BLE001
+        q.put(("err", repr(exc)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_band_all_to_all(world):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as ora
+
+    from paper_2511_08427_b200 import distributed as D
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = mp.start_processes(_a2a_worker, args=(world, _free_port(), q), nprocs=world, join=False,
+                               start_method="spawn")
+    res = q.get()
+    while not procs.join():
+        pass
+    assert res[0] == "ok", res
+    geom = _geom()
+    x = np.random.default_rng(0).standard_normal(geom.volume_shape).astype(np.float32).astype(np.float64)
+    mats = geom.matrix_array()
+    want = ora.forward_cone_3d(x, geom.volume_spacing, mats, geom.detector_shape, 0.45)
+    fdk = ora.fdk_cone_3d(want, mats, geom.sdd, geom.sid, geom.detector_spacing, geom.volume_shape,
+                          geom.volume_spacing, "shepp_logan")
+    slabs, angs = [], []
+    for rank, bands, per_chunks, slab, ang in res[1]:
+        z0, z1, r0, r1 = bands[rank]
+        for n_chunks, (band, order, ncalls) in per_chunks.items():
+            assert ncalls == n_chunks
+            assert sorted(order.tolist()) == list(range(geom.n_projections))
+            np.testing.assert_array_equal(order, D.received_view_order(geom.n_projections, world, n_chunks))
+            # exactly this rank's row band of every view, nothing else
+            assert band.shape == (geom.n_projections, r1 - r0, geom.detector_shape[1])
+            np.testing.assert_allclose(band, want[order, r0:r1], rtol=0, atol=1e-5 * np.abs(want).max())
+        slabs.append(slab)
+        if ang is not None:
+            angs.append(ang)
+    got = np.concatenate([s for _, s in sorted(slabs, key=lambda t: t[0])], axis=0)
+    assert ora.rel_l2(got, fdk) < 1e-5
+    if angs:
+        got = np.concatenate([s for _, s in sorted(angs, key=lambda t: t[0])], axis=0)
+        assert ora.rel_l2(got, fdk) < 1e-5
+
+
+def test_bands_move_fewer_bytes_than_all_gather():
+    """at the cfg4 geometry each rank receives its own row band,
+    <= 0.72 GB at N = 8 instead of the (N-1)/N x 3.02 GB an all-gather moves."""
+    import paper_2511_08427_b200 as tk
+    from paper_2511_08427_b200 import distributed as D
+
+    geom = tk.circular_cone_geometry((512,) * 3, (0.5,) * 3, (1024, 1024), (0.6, 0.6), 720, 2 * np.pi,
+                                     1200.0, 750.0)
+    for world in (2, 4, 8):
+        bands = D.slab_bands(geom, world)
+        # bytes that cross NVLink into each rank: its band rows of the other ranks' views
+        recv = [4 * 1024 * 720 * (r1 - r0) * (world - 1) / world for (_, _, r0, r1) in bands]
+        all_gather = (world - 1) / world * 4 * 720 * 1024 * 1024
+        assert max(recv) < all_gather * (0.45 if world == 2 else 0.32)
+        if world == 8:
+            assert max(recv) <= 0.72e9
+        assert [b[:2] for b in bands] == [D.shard_bounds(512, world, r) for r in range(world)]
+
+
+class _Work:
+    def __init__(self):
+        self.waited = False
+
+    def wait(self):
+        self.waited = True
+
+
+def test_nccl_branches_with_stubbed_collectives(monkeypatch):
+    """The NCCL code paths of gather_views and exchange_row_bands, with the
+    collectives stubbed by their single-process semantics (rank 0 of 2, the
+    peer holding the same data)."""
+    from paper_2511_08427_b200 import distributed as D
+
+    monkeypatch.setattr(D, "_backend", lambda: "nccl")
+    calls = {}
+
+    def fake_all_gather_into_tensor(out, inp, group=None):
+        calls["ag"] = (tuple(out.shape), tuple(inp.shape))
+        out.copy_(torch.cat([inp, inp + 100]))
+
+    works = []
+
+    def fake_all_to_all_single(out, inp, out_splits, in_splits, group=None, async_op=False):
+        calls.setdefault("a2a", []).append((list(out_splits), list(in_splits), async_op))
+        assert sum(out_splits) == out.numel() and sum(in_splits) == inp.numel()
+        # peer sends what we send to ourselves (same band rows, same counts)
+        chunks = list(torch.split(inp, in_splits))
+        out.copy_(torch.cat([chunks[0], chunks[0]]))
+        w = _Work()
+        works.append(w)
+        return w
+
+    monkeypatch.setattr(D.dist, "all_gather_into_tensor", fake_all_gather_into_tensor)
+    monkeypatch.setattr(D.dist, "all_to_all_single", fake_all_to_all_single)
+    loc = torch.arange(3 * 2 * 2, dtype=torch.float32).reshape(3, 2, 2)
+    full = D.gather_views(loc, [3, 3])
+    assert calls["ag"] == ((6, 2, 2), (3, 2, 2))
+    assert torch.equal(full[:3], loc) and torch.equal(full[3:], loc + 100)
+    # uneven counts: padded blocks, then cropped
+    full = D.gather_views(loc[:2].contiguous(), [2, 1])
+    assert full.shape == (3, 2, 2) and torch.equal(full[:2], loc[:2])
+    # row-band exchange: rank 0 owns rows [0, 1), rank 1 rows [1, 2)
+    bands = [(0, 1, 0, 1), (1, 2, 1, 2)]
+    out = torch.empty(6, 1, 2)
+    work, send = D.exchange_row_bands(loc, [3, 3], bands, 0, out, async_op=True)
+    assert calls["a2a"][-1] == ([6, 6], [6, 6], True) and work is works[-1]
+    assert torch.equal(out[:3], loc[:, 0:1]) and torch.equal(out[3:], loc[:, 0:1])
+    assert send.numel() == 12
