@@ -88,6 +88,12 @@ int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz,
                        double sy, double sx, const double *sources,
                        const double *minv, int n_views, int rows, int cols,
                        double step, float *out, void *stream);
+/* Which forward kernel tk_forward_cone_3d runs for this scan (host-only query,
+ * no device work): 1 = the z-mirror-pair kernel (every view z-mirror
+ * symmetric -- circular orbits with the principal row at (R-1)/2 -- and the
+ * volume fits its layout), 0 = the general ray-per-thread kernel. */
+int tk_forward_cone_3d_path(const double *sources, const double *minv, int n_views, int rows,
+                            int cols, int nz, int ny, int nx);
 /* Forward-projection plan (no reference counterpart): the per-volume
  * preprocessing of tk_forward_cone_3d (zero-margin quad-tap copies of the
  * volume in two orientations) done once, then any number of view blocks

@@ -2406,9 +2406,7 @@ static int fp_plan_project(const FpPlan &pl, const double *sources, const double
 static int launch_fp4(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                       const double *sources, const double *minv, int n_views, int rows, int cols,
                       double step, float *out, cudaStream_t st) {
-  const char *me = getenv("TK_FP_MIRROR");  // 0: never use the z-mirror-pair kernel
-  if (fp_algo() == FpAlgo::kLdg4z && !(me && !atoi(me)) && fp_mirror_fits(nz, ny, nx) &&
-      views_z_mirror(sources, minv, n_views, rows))
+  if (fp_use_mirror(sources, minv, n_views, rows, nz, ny, nx))
     return launch_fp_mirror(vol, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, out, st);
   FpPlan plan;
   int rc = fp_plan_create(vol, nz, ny, nx, sz, sy, sx, &plan, st);
@@ -2465,11 +2463,64 @@ static int launch_fp2(const float *vol, int nz, int ny, int nx, double sz, doubl
 }
 
 // A^T y by quad scatter (cone_fp_adjoint4_kernel) + fold (unquad_tiled_kernel).
-// Deterministic A^T: fixed-point scale 2^e from max |y| so that no tap sum can
-// overflow int64 (contribution <= |y| step, < 512 V contributions per tap).
+// Upper bound on the number of step-sized contributions one voxel tap can
+// receive over all views of a forward-projection transpose: per view, the rays
+// that can pass within the tap's support (a ball of radius rho = sqrt(3) s_max
+// around it) times the samples each such ray places in it.  Rays diverge from
+// the source, so at distance >= dmin (source to the volume box) adjacent
+// pixels' rays are >= dmin * alpha apart, alpha = the smallest angle between
+// adjacent pixels' rays, attained at a detector corner for a flat detector
+// (halved for safety).  Returns +inf when a source lies inside the box.
+static double fp_adjoint_tap_count_bound(const double *sources, const double *minv, int n_views, int rows, int cols,
+                                         int nz, int ny, int nx, double sz, double sy, double sx, double step) {
+  const double h[3] = {(nx + 1) * sx / 2.0, (ny + 1) * sy / 2.0, (nz + 1) * sz / 2.0};
+  const double rho = std::sqrt(3.0) * std::max(sx, std::max(sy, sz));
+  const double samples = 2.0 * rho / step + 2.0;
+  double total = 0.0;
+  for (int i = 0; i < n_views; ++i) {
+    const double *s = sources + 3 * i, *m = minv + 9 * i;
+    double d2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double e = std::max(0.0, std::fabs(s[k]) - h[k]);
+      d2 += e * e;
+    }
+    const double dmin = std::sqrt(d2);
+    if (!(dmin > 0.0)) return INFINITY;
+    auto dir = [&](double c, double r, double out[3]) {
+      for (int k = 0; k < 3; ++k) out[k] = m[3 * k] * c + m[3 * k + 1] * r + m[3 * k + 2];
+      const double n = std::sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
+      for (int k = 0; k < 3; ++k) out[k] /= n;
+    };
+    auto angle = [](const double a[3], const double b[3]) {
+      const double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
+      return std::atan2(std::sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
+    };
+    double au = INFINITY, av = INFINITY;
+    for (int cc = 0; cc < 2; ++cc)
+      for (int rr = 0; rr < 2; ++rr) {
+        const double c = cc ? cols - 1 : 0, r = rr ? rows - 1 : 0;
+        double d[3], du[3], dv[3];
+        dir(c, r, d);
+        dir(c + (cc ? -1 : 1), r, du);
+        dir(c, r + (rr ? -1 : 1), dv);
+        au = std::min(au, angle(d, du));
+        av = std::min(av, angle(d, dv));
+      }
+    au *= 0.5;
+    av *= 0.5;
+    const double nu = cols > 1 ? 2.0 * rho / (dmin * au) + 2.0 : 1.0;
+    const double nv = rows > 1 ? 2.0 * rho / (dmin * av) + 2.0 : 1.0;
+    total += nu * nv * samples;
+  }
+  return total;
+}
+
+// Deterministic A^T: fixed-point scale 2^e from max |y| and the geometry's tap
+// contribution bound, so that no tap sum can overflow int64 (each contribution
+// <= |y| step).
 static int launch_fp_adjoint_det(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
                                  const std::vector<Fp2View> &hv, Scratch &dviews, int n_views, int rows, int cols,
-                                 double step, float *vol, cudaStream_t st) {
+                                 double step, double tap_count, float *vol, cudaStream_t st) {
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   const long long nsino = (long long)n_views * rows * cols;
@@ -2488,7 +2539,9 @@ static int launch_fp_adjoint_det(const float *sino, int nz, int ny, int nx, doub
     TK_TRY_CUDA(cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nz * ny * nx, st));
     return std::isfinite(ymax) ? TK_OK : fail_arg("tk_forward_cone_3d_adjoint: non-finite sinogram");
   }
-  const double bound = (double)ymax * step * 512.0 * n_views;
+  if (!std::isfinite(tap_count))
+    return fail_arg("tk_forward_cone_3d_adjoint: deterministic mode needs every source outside the volume");
+  const double bound = (double)ymax * step * tap_count;
   const int e = std::min(100, (int)std::floor(62.0 - std::log2(bound)));
   const float scale = std::ldexp(1.0f, e);
   TK_TRY_CUDA(qA.alloc(32 * ncell, st));
@@ -2518,7 +2571,10 @@ static int launch_fp_adjoint4(const float *sino, int nz, int ny, int nx, double 
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
   if (deterministic)
-    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, hv, dviews, n_views, rows, cols, step, vol, st);
+    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, hv, dviews, n_views, rows, cols, step,
+                                 fp_adjoint_tap_count_bound(sources, minv, n_views, rows, cols, nz, ny, nx, sz, sy,
+                                                            sx, step),
+                                 vol, st);
   TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   if (zfast) {

@@ -88,6 +88,7 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
 // z-mirror-pair forward projector (tk_fp_mirror.cu): circular-orbit scans.
 bool views_z_mirror(const double *sources, const double *minv, int n_views, int rows);
 bool fp_mirror_fits(int nz, int ny, int nx);
+bool fp_use_mirror(const double *sources, const double *minv, int n_views, int rows, int nz, int ny, int nx);
 int launch_fp_mirror(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                      const double *sources, const double *minv, int n_views, int rows, int cols, double step,
                      float *out, cudaStream_t st);

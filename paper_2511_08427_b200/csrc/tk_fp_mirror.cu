@@ -204,6 +204,13 @@ bool fp_mirror_fits(int nz, int ny, int nx) {
   return mirror_layout(nz, nx).ok && (unsigned long long)(ny + 2 * kFpMargin) * kMirS < (1ull << 32);
 }
 
+bool fp_use_mirror(const double *sources, const double *minv, int n_views, int rows, int nz, int ny, int nx) {
+  const char *me = getenv("TK_FP_MIRROR");  // 0: never use the z-mirror-pair kernel
+  const char *algo = getenv("TK_FP_ALGO");  // only the default algorithm has a mirror form
+  if ((me && !atoi(me)) || (algo && strcmp(algo, "ldg4z"))) return false;
+  return fp_mirror_fits(nz, ny, nx) && views_z_mirror(sources, minv, n_views, rows);
+}
+
 int launch_fp_mirror(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                      const double *sources, const double *minv, int n_views, int rows, int cols, double step,
                      float *out, cudaStream_t st) {
@@ -238,3 +245,10 @@ int launch_fp_mirror(const float *vol, int nz, int ny, int nx, double sz, double
 }
 
 }  // namespace tk
+
+extern "C" int tk_forward_cone_3d_path(const double *sources, const double *minv, int n_views, int rows, int cols,
+                                       int nz, int ny, int nx) {
+  (void)cols;
+  if (!sources || !minv || n_views < 1 || rows < 1 || nz < 1 || ny < 1 || nx < 1) return 0;
+  return tk::fp_use_mirror(sources, minv, n_views, rows, nz, ny, nx) ? 1 : 0;
+}

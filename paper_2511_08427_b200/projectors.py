@@ -118,6 +118,19 @@ def fp_tensor(vol: torch.Tensor, geom, step: float, out: torch.Tensor | None = N
     raise TypeError(f"unsupported geometry {type(geom).__name__}")
 
 
+def forward_kernel_path(geom: GeometryCone3D) -> str:
+    """Which cone forward kernel `fp_tensor` runs for this geometry (host-only
+    query of tk_forward_cone_3d_path): "mirror" -- one thread marches a ray and
+    its z-mirror image (circular orbits) -- or "general"."""
+    src, minv = geom.ray_constants
+    (src, psrc), (minv, pminv) = _lib.host_f64(src), _lib.host_f64(minv)
+    nz, ny, nx = geom.volume_shape
+    rows, cols = geom.detector_shape
+    lib = _lib.load()
+    return "mirror" if lib.tk_forward_cone_3d_path(psrc, pminv, geom.n_projections, rows, cols, nz, ny, nx) \
+        else "general"
+
+
 class ForwardProjectionPlan:
     """A cone-beam volume prepared once (tk_fp_plan_create) and projected in
     view blocks (tk_fp_plan_project) -- used to overlap per-block D2H copies

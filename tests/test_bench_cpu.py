@@ -29,15 +29,19 @@ def test_reference_arm_prints_contract_line():
     assert "workload" in d["config"]
 
 
-def test_gather_roofline_fractions():
+def test_roofline_names_the_binding_bound():
+    """`roofline` puts the dominant kernel against the L1 load path (the bound
+    that binds a gather kernel), and reports its HBM position separately on
+    algorithmic HBM bytes -- never L1-served bytes over the HBM peak."""
     sys.path.insert(0, str(ROOT))
     import bench
 
-    g = bench.gather_roofline(32.0 * 1e12, 1000.0, 16.0 * 1e12, 500.0, {"sm_mhz": 1965.0})
-    # peak = measured LDG.128 bytes/clk/SM (profiles/l1_peak_*.json) x 148 SMs x clock
-    per_clk = json.loads(sorted((ROOT / "profiles").glob("l1_peak_*.json"))[-1].read_text())["ldg128_bytes_per_clk_sm"]
-    peak = per_clk * 148 * 1965.0 * 1e6 / 1e9
-    assert 120.0 <= per_clk <= 128.0 and "measured" in g["peak_source"]
-    assert g["peak"] == pytest.approx(peak, abs=0.1)
-    assert g["forward"]["achieved"] == pytest.approx(32.0e12 / 1.0 / 1e9, abs=0.1)
-    assert g["back"]["frac"] == pytest.approx(16.0e12 / 0.5 / 1e9 / peak, rel=1e-3)
+    l1 = {"ldg128_gbs": 36000.0, "lds32_gbs": 31000.0, "source": "test"}
+    r = bench.roofline(samples=1e12, fp_ms=1000.0, fp_views=720, bp_updates=1e11, bp_ms=100.0, l1=l1)
+    assert r["bound"] == "l1_load_path" and r["unit"] == "GB/s" and r["peak"] == 36000.0
+    assert r["achieved"] == pytest.approx(32.0e12 / 1.0 / 1e9, abs=0.1)
+    assert r["frac"] == pytest.approx(32.0e3 / 36000.0, rel=1e-3)
+    alg = 4.0 * (512 ** 3 + 720 * 1024 * 1024)
+    assert r["hbm"]["algorithmic_bytes_per_launch"] == alg
+    assert r["hbm"]["frac"] == pytest.approx(alg / 1.0 / 1e9 / r["hbm"]["peak"], rel=1e-2)
+    assert r["back"]["frac"] == pytest.approx(16.0e11 / 0.1 / 1e9 / 36000.0, rel=1e-3)

@@ -695,6 +695,21 @@ def test_deterministic_cone_transpose(tk, oracle):
     assert torch.equal(a, c)
 
 
+def test_deterministic_transpose_many_rays_per_cell(tk, oracle):
+    """A detector far finer than the voxel grid (hundreds of rays per cell per
+    view) with a same-sign sinogram: the fixed-point scale comes from the
+    geometry's tap-contribution bound, so the int64 sums cannot wrap."""
+    from paper_2511_08427_b200.projectors import fp_adjoint_tensor
+
+    shape, sp = (6, 6, 6), (4.0, 4.0, 4.0)
+    geom = cone(tk, 6, 160, 0.25, 7, spacing=4.0)
+    y = np.ones((7, 160, 160))
+    a = fp_adjoint_tensor(T(y), geom, 0.5, deterministic=True)
+    want = oracle.forward_cone_3d_T(y, shape, sp, geom.matrix_array(), 0.5)
+    assert float(a.min()) >= 0.0
+    assert rel(a, want) < TOL
+
+
 def test_nondeterministic_transposes_follow_torch_determinism(tk):
     """Under torch.use_deterministic_algorithms(True) the atomic-only transposes raise
     (torch's convention), warn with warn_only=True, and the cone A^T switches to its
@@ -751,3 +766,40 @@ def test_bp_tma_z_block_knob(tk, monkeypatch, zb):
     got = tk.back_project(tk.Sinogram(y, (1.6, 1.5)), geom, True).data
     assert bool(torch.isfinite(got).all())
     assert rel(got, want.cpu().numpy()) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# z-mirror-pair forward projector (circular orbits)
+# ---------------------------------------------------------------------------
+
+
+class TestMirrorForward:
+    @pytest.mark.parametrize("shape,spacing,det,ds,views", [
+        ((64, 64, 64), (1.0, 1.0, 1.0), (96, 96), (1.6, 1.6), 40),        # even rows
+        ((33, 40, 21), (0.8, 1.1, 0.9), (31, 45), (1.9, 1.4), 17),        # odd rows / odd nz, ragged
+        ((20, 16, 16), (1.0, 1.0, 1.0), (7, 40), (2.5, 1.2), 9),          # detector narrower than the shadow
+        ((16, 16, 16), (1.0, 1.0, 1.0), (1, 24), (1.6, 1.6), 5),          # single (middle) row
+    ])
+    def test_matches_oracle_and_general_kernel(self, tk, oracle, monkeypatch, shape, spacing, det, ds, views):
+        from paper_2511_08427_b200.projectors import forward_kernel_path
+
+        geom = tk.circular_cone_geometry(shape, spacing, det, ds, views, 2 * np.pi, 1200.0, 750.0)
+        assert forward_kernel_path(geom) == "mirror"
+        x = np.random.default_rng(7).standard_normal(shape).astype(np.float32).astype(np.float64)
+        got = tk.forward_project(tk.Volume(x, spacing), geom).data
+        want = oracle.forward_cone_3d(x, spacing, geom.matrix_array(), det, 0.5 * min(spacing))
+        assert rel(got, want) < TOL
+        monkeypatch.setenv("TK_FP_MIRROR", "0")
+        general = tk.forward_project(tk.Volume(x, spacing), geom).data
+        assert rel(got, general.cpu().numpy()) < 2e-6
+        # the direct rows are the general kernel's rays bit for bit (same cells, same arithmetic)
+        half = det[0] // 2
+        assert torch.equal(got[:, :half], general[:, :half])
+
+    @pytest.mark.parametrize("cfg", ["4x3", "8x1", "8x2"])
+    def test_launch_configurations(self, tk, oracle, monkeypatch, cfg):
+        monkeypatch.setenv("TK_FPM_CFG", cfg)
+        geom = tk.circular_cone_geometry((48,) * 3, (1.0,) * 3, (64, 80), (1.6, 1.6), 19, 2 * np.pi, 1200.0, 750.0)
+        x = oracle.shepp_logan_3d((48,) * 3)
+        got = tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data
+        assert rel(got, oracle.forward_cone_3d(x, (1, 1, 1), geom.matrix_array(), (64, 80), 0.5)) < TOL
