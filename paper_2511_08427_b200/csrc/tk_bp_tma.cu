@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kBtStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBtConsumers / 32);
+      mbar_init(&empty[s], kBtConsumers);  // every consumer thread arrives after its last read of the stage
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -214,8 +214,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    mbar_arrive(&empty[s]);  // release: this thread's reads of meta[s] and the tile happen before the refill
   }
   if (!active) return;
 #pragma unroll

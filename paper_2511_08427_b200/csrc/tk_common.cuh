@@ -114,4 +114,11 @@ __device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsign
   return d;
 }
 
+// 16-byte vector reduction into global memory (REDG.E.ADD.F32x4): one L2 atomic
+// operation for four fp32 adds.
+__device__ __forceinline__ void red_add_v4(float4 *p, const float4 &v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 }  // namespace tk

@@ -1,5 +1,6 @@
 // tk_cone_fp.cuh -- per-view constants and per-ray set-up shared by the cone
-// forward projectors (tk_cone.cu, tk_fp_slab.cu).
+// forward projector (tk_fp.cu), its texture comparison kernels (tk_fp_tex.cu)
+// and its transpose (tk_fp_adjoint.cu).
 #pragma once
 
 #include "tk_common.cuh"
@@ -14,11 +15,7 @@ struct ConeRayView {  // per-view forward constants (float64): source, M^-1
 // Zero margin (voxels) of the forward projectors' orientation copies.
 constexpr int kFpMargin = 2;
 
-struct Fp2View {
-  ConeRayView ray;
-  int swap;       // 1: use the y-fastest copy (x and y exchanged)
-  int face_copy;  // 1: pick the copy per ray from its entry face (cone_fp4_kernel)
-};
+
 
 
 // ---------------------------------------------------------------------------
@@ -85,12 +82,12 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
   return true;
 }
 
-// z-mirror-pair forward projector (tk_fp_mirror.cu): circular-orbit scans.
+// tk_fp.cu: z-mirror symmetry test of a scan and the default launch.
 bool views_z_mirror(const double *sources, const double *minv, int n_views, int rows);
-bool fp_mirror_fits(int nz, int ny, int nx);
 bool fp_use_mirror(const double *sources, const double *minv, int n_views, int rows, int nz, int ny, int nx);
-int launch_fp_mirror(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
-                     const double *sources, const double *minv, int n_views, int rows, int cols, double step,
-                     float *out, cudaStream_t st);
+// tk_fp_tex.cu: texture-unit comparison kernels (hw: hardware trilinear filtering).
+int launch_fp_tex(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx, const double *sources,
+                  const double *minv, int n_views, int rows, int cols, double step, bool hw, float *out,
+                  cudaStream_t st);
 
 }  // namespace tk

@@ -1,0 +1,390 @@
+// tk_fp_adjoint.cu -- the exact transpose A^T of the ray-driven cone forward
+// projector (matched adjoint; reference autodiff.py:59-68 asks for the
+// transposed operator, the reference itself pairs A with the voxel-driven B).
+//
+// The forward march transposed (same rays, set-up and sample positions as
+// tk_fp.cu / _kernels.py:254-278, 117-157): each sample's 8 trilinear weights
+// times y * seg are accumulated in registers while the ray stays in one cell
+// and flushed as 16-byte vector reductions (REDG.E.ADD.F32x4, one per 4 taps)
+// into z-fastest tap quads; tiled folds sum the 4 quads holding each voxel's
+// tap back into the (z, y, x) volume.  fp32 atomics: summation order is not
+// deterministic.  Deterministic mode: 64-bit fixed-point quads with integer
+// atomics (associative: bit-reproducible), scale chosen from max |y| and a
+// geometric bound on the contributions per tap so no sum can overflow.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "tk_cone_fp.cuh"
+
+namespace tk {
+
+constexpr int kFpzRows = 8;  // detector rows per quarter-warp (one column)
+
+
+// z-fastest form of the quad scatter (the transpose of cone_fp4z_kernel, "red4z",
+// default): quarter = 8 rows of one column, so lanes flush together into
+// contiguous quads.  Two scatter buffers, one per horizontal row axis b:
+//   qy: Qz[y][x][z] += (w(z,x), w(z,x+1), w(z+1,x), w(z+1,x+1)) of row y,
+//   qx: Qx[x][y][z] += (w(z,y), w(z,y+1), w(z+1,y), w(z+1,y+1)) of row x;
+// a ray scatters into the buffer whose row axis is its major horizontal axis,
+// so most cell changes are row steps b -> b +- 1, where the new cell's near row
+// is the old cell's far row: that quad's accumulator is carried over in
+// registers and only the row left behind is flushed (one REDG.F32x4 instead of
+// two).
+// DET: fixed-point flush -- each quad component is rounded to an integer multiple of
+// 2^-e (scale = 2^e, exact) and added with 64-bit integer atomics into u64 quads.
+// Integer addition is associative, so the result does not depend on the order in
+// which rays flush: bit-reproducible (torch.use_deterministic_algorithms).
+__device__ __forceinline__ void red_add_fx4(unsigned long long *p, const float4 &v, float scale) {
+  atomicAdd(p, (unsigned long long)__float2ll_rn(v.x * scale));
+  atomicAdd(p + 1, (unsigned long long)__float2ll_rn(v.y * scale));
+  atomicAdd(p + 2, (unsigned long long)__float2ll_rn(v.z * scale));
+  atomicAdd(p + 3, (unsigned long long)__float2ll_rn(v.w * scale));
+}
+
+template <int MINB, bool DET = false>
+__global__ void __launch_bounds__(128, MINB)
+    cone_fp_adjoint4z_kernel(const float *__restrict__ sino, void *__restrict__ qy_, void *__restrict__ qx_,
+                             int nx, int ny, int nz, double sx, double sy, double sz,
+                             const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
+                             float scale) {
+  constexpr int kCols = 16;
+  const int ncb = (cols + kCols - 1) / kCols;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views);
+  const int rb = (int)(bt / n_views);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = cb * kCols + warp * 4 + (lane >> 3);
+  const int r = rb * kFpzRows + (lane & 7);
+  if (c >= cols || r >= rows) return;
+  const float y = __ldg(sino + ((long long)v * rows + r) * cols + c);
+  if (y == 0.f) return;
+  RaySetup rs;
+  if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
+  const bool xrow = fabsf(rs.gx) > fabsf(rs.gy);  // major horizontal axis (cells per step)
+  void *qv = xrow ? qx_ : qy_;
+  auto flush = [&](unsigned cidx, const float4 &v) {  // quad cidx += v
+    if (DET)
+      red_add_fx4(static_cast<unsigned long long *>(qv) + 4ull * cidx, v, scale);
+    else
+      red_add_v4(static_cast<float4 *>(qv) + cidx, v);
+  };
+  const float ea = (xrow ? rs.ey : rs.ex) + (kFpMargin - 1), eb = (xrow ? rs.ex : rs.ey) + (kFpMargin - 1);
+  const float ez = rs.ez + (kFpMargin - 1);
+  const float ga = xrow ? rs.gy : rs.gx, gb = xrow ? rs.gx : rs.gy, gz = rs.gz;
+  const unsigned pz = (unsigned)(nz + 2 * kFpMargin);
+  const unsigned sas = pz, sbs = (unsigned)((xrow ? ny : nx) + 2 * kFpMargin) * pz;  // a and b strides
+  const unsigned bias = kFloorBits * (1u + sas + sbs);
+  const float g = y * (float)step;
+  float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+  unsigned cell = 0u;
+  bool open = false;
+  auto sample = [&](float kk, float gs) {
+    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
+    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
+    const unsigned id = __float_as_uint(xb) * sbs + (__float_as_uint(xa) * sas + __float_as_uint(xz));
+    if (id != cell) {
+      const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (open) {
+        const unsigned c0 = cell - bias;
+        const unsigned d = id - cell;
+        if (d == sbs) {  // row b -> b + 1: the far row becomes the near row
+          flush(c0, lo);
+          lo = hi;
+          hi = zero;
+        } else if (d == 0u - sbs) {  // row b -> b - 1: the near row becomes the far row
+          flush(c0 + sbs, hi);
+          hi = lo;
+          lo = zero;
+        } else {
+          flush(c0, lo);
+          flush(c0 + sbs, hi);
+          lo = hi = zero;
+        }
+      }
+      open = true;
+      cell = id;
+    }
+    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
+    const float g1 = gs * wb, g0 = gs - g1;
+    const float l1 = g0 * wz, l0 = g0 - l1, h1 = g1 * wz, h0 = g1 - h1;
+    const float l0a = l0 * wa, l1a = l1 * wa, h0a = h0 * wa, h1a = h1 * wa;
+    lo.x += l0 - l0a;
+    lo.y += l0a;
+    lo.z += l1 - l1a;
+    lo.w += l1a;
+    hi.x += h0 - h0a;
+    hi.y += h0a;
+    hi.z += h1 - h1a;
+    hi.w += h1a;
+  };
+  float kf = 0.5f;
+  const int nfull = rs.n - 1;
+  for (int k = 0; k < nfull; ++k, kf += 1.f) sample(kf, g);
+  sample((float)nfull + 0.5f * rs.last, g * rs.last);
+  flush(cell - bias, lo);
+  flush(cell - bias + sbs, hi);
+}
+
+// deterministic fold: vol[z][y][x] = 2^-e (sum of the 8 fixed-point taps of both
+// scatter buffers) -- integer sums, one rounding to float
+__global__ void __launch_bounds__(256) unquad_fx_kernel(const unsigned long long *__restrict__ qy,
+                                                        const unsigned long long *__restrict__ qx, int nz, int ny,
+                                                        int nx, double inv_scale, float *__restrict__ vol) {
+  constexpr int m = kFpMargin;
+  const long long pz = nz + 2 * m, px = nx + 2 * m, py = ny + 2 * m;
+  const long long n = (long long)nz * ny * nx;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long long)nx * ny));
+    const long long zp = z + m, yp = y + m, xp = x + m;
+    // qy: Qz[y][x][z] taps (z,x),(z,x+1),(z+1,x),(z+1,x+1) of row y
+    auto Y = [&](long long yy, long long xx, long long zz, int c) { return (long long)qy[4 * ((yy * px + xx) * pz + zz) + c]; };
+    // qx: Qx[x][y][z] taps (z,y),(z,y+1),(z+1,y),(z+1,y+1) of row x
+    auto X = [&](long long xx, long long yy, long long zz, int c) { return (long long)qx[4 * ((xx * py + yy) * pz + zz) + c]; };
+    const long long t = Y(yp, xp, zp, 0) + Y(yp, xp - 1, zp, 1) + Y(yp, xp, zp - 1, 2) + Y(yp, xp - 1, zp - 1, 3) +
+                        X(xp, yp, zp, 0) + X(xp, yp - 1, zp, 1) + X(xp, yp, zp - 1, 2) + X(xp, yp - 1, zp - 1, 3);
+    vol[i] = (float)((double)t * inv_scale);
+  }
+}
+
+__global__ void absmax_kernel(const float *__restrict__ x, long long n, unsigned *__restrict__ out) {
+  unsigned m = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(__ldg(x + i))));  // non-negative floats order as integers
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// vol += fold of the x-row scatter quads qx: the tap at padded (z, y, x) is
+// Qx[x][y][z].x + Qx[x][y-1][z].y + Qx[x][y][z-1].z + Qx[x][y-1][z-1].w.
+// 32 (z) x 32 (x) tiles of one y: quad reads along z, volume writes along x.
+__global__ void __launch_bounds__(256) unquad_zx_kernel(const float4 *__restrict__ q, int nz, int ny, int nx,
+                                                        float *__restrict__ vol) {
+  __shared__ float4 tq[2][32][33];  // [y row: 0 = y-1, 1 = y][x - x0][z - z0 + 1]
+  __shared__ float res[32][33];     // [z - z0][x - x0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, py = ny + 2 * m;
+  const int z0 = blockIdx.x * 32, x0 = blockIdx.y * 32, y = blockIdx.z;  // real voxel coordinates
+  for (int e = threadIdx.x; e < 2 * 32 * 33; e += 256) {
+    const int h = e / (32 * 33), f = e % (32 * 33);
+    const int dz = f % 33, dx = f / 33;
+    const int zi = z0 + m - 1 + dz, xi = x0 + m + dx, yi = y + m - 1 + h;  // padded cell coordinates
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zi < pz && x0 + dx < nx) val = q[((long long)xi * py + yi) * pz + zi];
+    tq[h][dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8)
+    res[tz][tx] = tq[1][tx][tz + 1].x + tq[0][tx][tz + 1].y + tq[1][tx][tz].z + tq[0][tx][tz].w;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int dx = e & 31, dz = e >> 5;
+    const int x = x0 + dx, z = z0 + dz;
+    if (x < nx && z < nz) vol[((long long)z * ny + y) * nx + x] += res[dz][dx];
+  }
+}
+
+// vol = fold of the z-fastest scatter quads: the tap at padded (z, y, x) is
+// Qz[y][x][z].x + Qz[y][x-1][z].y + Qz[y][x][z-1].z + Qz[y][x-1][z-1].w.
+// 32 (z) x 32 (x) tiles of one y row: quad reads along z, volume writes along x.
+__global__ void __launch_bounds__(256) unquad_z_kernel(const float4 *__restrict__ q, int nz, int ny, int nx,
+                                                       float *__restrict__ vol) {
+  __shared__ float4 tq[33][33];  // [x - x0 + 1][z - z0 + 1]
+  __shared__ float res[32][33];  // [z - z0][x - x0]
+  constexpr int m = kFpMargin;
+  const int pz = nz + 2 * m, px = nx + 2 * m;
+  const int z0 = blockIdx.x * 32, x0 = blockIdx.y * 32, y = blockIdx.z;  // real voxel coordinates
+  const long long row = (long long)(y + m) * px;
+  for (int e = threadIdx.x; e < 33 * 33; e += 256) {
+    const int dz = e % 33, dx = e / 33;
+    const int zi = z0 + m - 1 + dz, xi = x0 + m - 1 + dx;  // padded cell coordinates
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zi < pz && xi < px) val = q[(row + xi) * pz + zi];
+    tq[dx][dz] = val;
+  }
+  __syncthreads();
+  const int tz = threadIdx.x & 31;
+  for (int tx = threadIdx.x >> 5; tx < 32; tx += 8)
+    res[tz][tx] = tq[tx + 1][tz + 1].x + tq[tx][tz + 1].y + tq[tx + 1][tz].z + tq[tx][tz].w;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int dx = e & 31, dz = e >> 5;
+    const int x = x0 + dx, z = z0 + dz;
+    if (x < nx && z < nz) vol[((long long)z * ny + y) * nx + x] = res[dz][dx];
+  }
+}
+
+
+// Upper bound on the number of step-sized contributions one voxel tap can
+// receive over all views of a forward-projection transpose: per view, the rays
+// that can pass within the tap's support (a ball of radius rho = sqrt(3) s_max
+// around it) times the samples each such ray places in it.  Rays diverge from
+// the source, so at distance >= dmin (source to the volume box) adjacent
+// pixels' rays are >= dmin * alpha apart, alpha = the smallest angle between
+// adjacent pixels' rays, attained at a detector corner for a flat detector
+// (halved for safety).  Returns +inf when a source lies inside the box.
+static double fp_adjoint_tap_count_bound(const double *sources, const double *minv, int n_views, int rows, int cols,
+                                         int nz, int ny, int nx, double sz, double sy, double sx, double step) {
+  const double h[3] = {(nx + 1) * sx / 2.0, (ny + 1) * sy / 2.0, (nz + 1) * sz / 2.0};
+  const double rho = std::sqrt(3.0) * std::max(sx, std::max(sy, sz));
+  const double samples = 2.0 * rho / step + 2.0;
+  double total = 0.0;
+  for (int i = 0; i < n_views; ++i) {
+    const double *s = sources + 3 * i, *m = minv + 9 * i;
+    double d2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double e = std::max(0.0, std::fabs(s[k]) - h[k]);
+      d2 += e * e;
+    }
+    const double dmin = std::sqrt(d2);
+    if (!(dmin > 0.0)) return INFINITY;
+    auto dir = [&](double c, double r, double out[3]) {
+      for (int k = 0; k < 3; ++k) out[k] = m[3 * k] * c + m[3 * k + 1] * r + m[3 * k + 2];
+      const double n = std::sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
+      for (int k = 0; k < 3; ++k) out[k] /= n;
+    };
+    auto angle = [](const double a[3], const double b[3]) {
+      const double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
+      return std::atan2(std::sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
+    };
+    double au = INFINITY, av = INFINITY;
+    for (int cc = 0; cc < 2; ++cc)
+      for (int rr = 0; rr < 2; ++rr) {
+        const double c = cc ? cols - 1 : 0, r = rr ? rows - 1 : 0;
+        double d[3], du[3], dv[3];
+        dir(c, r, d);
+        dir(c + (cc ? -1 : 1), r, du);
+        dir(c, r + (rr ? -1 : 1), dv);
+        au = std::min(au, angle(d, du));
+        av = std::min(av, angle(d, dv));
+      }
+    au *= 0.5;
+    av *= 0.5;
+    const double nu = cols > 1 ? 2.0 * rho / (dmin * au) + 2.0 : 1.0;
+    const double nv = rows > 1 ? 2.0 * rho / (dmin * av) + 2.0 : 1.0;
+    total += nu * nv * samples;
+  }
+  return total;
+}
+
+// Deterministic A^T: fixed-point scale 2^e from max |y| and the geometry's tap
+// contribution bound, so that no tap sum can overflow int64 (each contribution
+// <= |y| step).
+static int launch_fp_adjoint_det(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
+                                 Scratch &dviews, int n_views, int rows, int cols,
+                                 double step, double tap_count, float *vol, cudaStream_t st) {
+  constexpr int m2 = 2 * kFpMargin;
+  const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  const long long nsino = (long long)n_views * rows * cols;
+  Scratch dmax, qA, qB;
+  TK_TRY_CUDA(dmax.alloc(sizeof(unsigned), st));
+  TK_TRY_CUDA(cudaMemsetAsync(dmax.ptr, 0, sizeof(unsigned), st));
+  absmax_kernel<<<(unsigned)std::min<long long>(ceil_div(nsino, 256), (long long)sm_count() * 8), 256, 0, st>>>(
+      sino, nsino, dmax.as<unsigned>());
+  TK_LAUNCHED("absmax_kernel");
+  unsigned bits = 0;
+  TK_TRY_CUDA(cudaMemcpyAsync(&bits, dmax.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  TK_TRY_CUDA(cudaStreamSynchronize(st));
+  float ymax;
+  std::memcpy(&ymax, &bits, sizeof(float));
+  if (!(ymax > 0.f) || !std::isfinite(ymax)) {
+    TK_TRY_CUDA(cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nz * ny * nx, st));
+    return std::isfinite(ymax) ? TK_OK : fail_arg("tk_forward_cone_3d_adjoint: non-finite sinogram");
+  }
+  if (!std::isfinite(tap_count))
+    return fail_arg("tk_forward_cone_3d_adjoint: deterministic mode needs every source outside the volume");
+  const double bound = (double)ymax * step * tap_count;
+  const int e = std::min(100, (int)std::floor(62.0 - std::log2(bound)));
+  const float scale = std::ldexp(1.0f, e);
+  TK_TRY_CUDA(qA.alloc(32 * ncell, st));
+  TK_TRY_CUDA(qB.alloc(32 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, 32 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, 32 * ncell, st));
+  const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+  if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  cone_fp_adjoint4z_kernel<8, true><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
+                                                                   dviews.as<ConeRayView>(), rows, cols, n_views, step,
+                                                                   scale);
+  TK_LAUNCHED("cone_fp_adjoint4z_kernel");
+  const long long nv = (long long)nz * ny * nx;
+  unquad_fx_kernel<<<(unsigned)std::min<long long>(ceil_div(nv, 256), (long long)sm_count() * 16), 256, 0, st>>>(
+      qA.as<unsigned long long>(), qB.as<unsigned long long>(), nz, ny, nx, std::ldexp(1.0, -e), vol);
+  TK_LAUNCHED("unquad_fx_kernel");
+  return TK_OK;
+}
+
+static int launch_fp_adjoint(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
+                             const double *sources, const double *minv, int n_views, int rows, int cols, double step,
+                             bool deterministic, float *vol, cudaStream_t st) {
+  std::vector<ConeRayView> hv(n_views);
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].minv[j] = minv[9 * i + j];
+  }
+  Scratch dviews, qA, qB;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
+  constexpr int m2 = 2 * kFpMargin;
+  const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
+  if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
+  if (deterministic)
+    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, dviews, n_views, rows, cols, step,
+                                 fp_adjoint_tap_count_bound(sources, minv, n_views, rows, cols, nz, ny, nx, sz, sy,
+                                                            sx, step),
+                                 vol, st);
+  TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
+  const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+  if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
+                                                             dviews.as<ConeRayView>(), rows, cols, n_views, step, 1.f);
+  TK_LAUNCHED("cone_fp_adjoint4z_kernel");
+  unquad_z_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qA.as<float4>(), nz, ny, nx, vol);
+  TK_LAUNCHED("unquad_z_kernel");
+  unquad_zx_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qB.as<float4>(), nz, ny, nx, vol);
+  TK_LAUNCHED("unquad_zx_kernel");
+  return TK_OK;
+}
+
+}  // namespace tk
+
+using namespace tk;
+
+extern "C" {
+
+static int fp_adjoint_args(const float *sino, const float *vol_out, const double *sources, const double *minv, int nz,
+                           int ny, int nx, int n_views, int rows, int cols, double sx, double sy, double sz,
+                           double step) {
+  if (!sino || !vol_out || !sources || !minv) return fail_arg("tk_forward_cone_3d_adjoint: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1)
+    return fail_arg("tk_forward_cone_3d_adjoint: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0 && step > 0))
+    return fail_arg("tk_forward_cone_3d_adjoint: spacing/step must be > 0");
+  return TK_OK;
+}
+
+int tk_forward_cone_3d_adjoint_ex(const float *sino, int n_views, int rows, int cols, const double *sources,
+                                  const double *minv, int nz, int ny, int nx, double sz, double sy, double sx,
+                                  double step, int deterministic, float *vol_out, void *stream) {
+  clear_error();
+  const int rc = fp_adjoint_args(sino, vol_out, sources, minv, nz, ny, nx, n_views, rows, cols, sx, sy, sz, step);
+  if (rc != TK_OK) return rc;
+  return launch_fp_adjoint(sino, nz, ny, nx, sz, sy, sx, sources, minv, n_views, rows, cols, step, deterministic != 0,
+                           vol_out, as_stream(stream));
+}
+
+int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int cols, const double *sources,
+                               const double *minv, int nz, int ny, int nx, double sz, double sy, double sx, double step,
+                               float *vol_out, void *stream) {
+  return tk_forward_cone_3d_adjoint_ex(sino, n_views, rows, cols, sources, minv, nz, ny, nx, sz, sy, sx, step, 0,
+                                       vol_out, stream);
+}
+
+}  // extern "C"

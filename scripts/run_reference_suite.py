@@ -82,7 +82,9 @@ def main():
                                                      "test_acceptance.py")]
     rec = Recorder()
     t0 = time.time()
-    rc = pytest.main(["-q", "-p", "no:cacheprovider", "--rootdir", str(tests), *map(str, files), *extra],
+    # importlib mode: the two suites each have a test_acceptance.py (basename clash under rootdir-relative imports)
+    rc = pytest.main(["-q", "-p", "no:cacheprovider", "--import-mode=importlib", "--rootdir", str(tests),
+                      *map(str, files), *extra],
                      plugins=[rec])
     counts = {}
     for r in rec.results.values():

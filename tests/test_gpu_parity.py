@@ -406,9 +406,16 @@ def _poison(shape):
     del t
 
 
-@pytest.mark.parametrize("algo", ["ldg4m", "ldg4z", "ldg4zq", "ldg4p", "ldg4", "ldg8", "ldg2", "ldg", "tex"])
-def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
-    monkeypatch.setenv("TK_FP_ALGO", algo)
+FP_KNOBS = [{}, {"TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x1", "TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "8x2", "TK_FP_MIRROR": "1"},
+            {"TK_FP_ALGO": "tex"}]
+
+
+@pytest.mark.parametrize("knobs", FP_KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
+def test_fp_variants_match_oracle(tk, oracle, monkeypatch, knobs):
+    """Every forward-projector kernel / launch configuration against
+    the oracle on circular (mirror-eligible), helical and long orbits."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
     geom = tk.GeometryCone3D((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4),
                              tk.circular_trajectory_3d(17, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4)),
                              1200.0, 750.0)
@@ -435,23 +442,7 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, algo):
     assert rel(got, g.forward_cone_3d(x, (0.9, 1.1, 1.0), gl.matrix_array(), (30, 34), 0.45)) < TOL
 
 
-@pytest.mark.parametrize("face", ["1", "0"])
-def test_fp_orientation_copy_choice(tk, monkeypatch, face):
-    # per-ray (entry face) vs per-view copy choice: same taps and weights, only the
-    # order of the x / y lerps differs between the two copies (fp32 rounding)
-    geom = tk.circular_cone_geometry((40, 44, 36), (1.0, 0.9, 1.1), (48, 52), (1.6, 1.5), 23, 2 * np.pi,
-                                     1200.0, 750.0)
-    x = torch.randn(40, 44, 36, device="cuda")
-    monkeypatch.setenv("TK_FP_FACE", face)
-    got = tk.forward_project(tk.Volume(x, (1.0, 0.9, 1.1)), geom).data
-    monkeypatch.setenv("TK_FP_FACE", "0" if face == "1" else "1")
-    other = tk.forward_project(tk.Volume(x, (1.0, 0.9, 1.1)), geom).data
-    assert rel(got, other.cpu().numpy()) < 1e-6
-
-
-@pytest.mark.parametrize("algo", ["red4z", "red4", "scatter"])
-def test_fp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
-    monkeypatch.setenv("TK_FPT_ALGO", algo)
+def test_fp_transpose_matches_oracle(tk, oracle):
     shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
     hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
     for mats in (hel, tk.circular_trajectory_3d(13, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4))):
@@ -462,9 +453,7 @@ def test_fp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
         assert rel(got, want) < TOL
 
 
-@pytest.mark.parametrize("algo", ["red4", "scatter"])
-def test_bp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
-    monkeypatch.setenv("TK_BPT_ALGO", algo)
+def test_bp_transpose_matches_oracle(tk, oracle):
     shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
     hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
     x = np.random.default_rng(32).standard_normal(shape)
@@ -476,16 +465,9 @@ def test_bp_transpose_variants_match_oracle(tk, oracle, monkeypatch, algo):
             assert rel(got, want) < TOL
 
 
-def _set_bp_algo(monkeypatch, algo):
-    if algo == "quad8x1":  # quad kernel with the 8x1 quarter-warp voxel mapping
-        monkeypatch.setenv("TK_BP_Q42", "0")
-        algo = "quad"
-    monkeypatch.setenv("TK_BP_ALGO", algo)
-
-
-@pytest.mark.parametrize("algo", ["tma", "smem", "quad", "quad8x1", "coef", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["tma", "quad", "tex"])
 def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
-    _set_bp_algo(monkeypatch, algo)
+    monkeypatch.setenv("TK_BP_ALGO", algo)
     geom = cone(tk, 24, 36, 1.5, 19)
     y = np.random.default_rng(22).standard_normal((19, 36, 36))
     for w in (False, True):
@@ -497,11 +479,11 @@ def test_bp_variants_match_oracle(tk, oracle, golden, monkeypatch, algo):
     assert rel(tk.back_project(tk.Sinogram(g["yt"], (1.6, 1.6)), gt, True).data, g["bp_t"]) < TOL
 
 
-@pytest.mark.parametrize("algo", ["tma", "smem", "quad", "quad8x1", "coef", "ldg", "tex"])
+@pytest.mark.parametrize("algo", ["tma", "quad", "tex"])
 def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
     """Sharded building block: a z-slab from a cropped detector row band equals
     the same slab of the full back projection."""
-    _set_bp_algo(monkeypatch, algo)
+    monkeypatch.setenv("TK_BP_ALGO", algo)
     from paper_2511_08427_b200 import distributed as D
     from paper_2511_08427_b200.projectors import bp_cone_tensor_ex
 
@@ -517,9 +499,9 @@ def test_bp_row_band_zslab(tk, oracle, monkeypatch, algo):
             assert rel(slab, full[z0:z1].cpu().numpy()) < 1e-5  # fp32 row-shift rounding
 
 
-@pytest.mark.parametrize("algo", ["smem", "tma"])
+@pytest.mark.parametrize("algo", ["tma"])
 @pytest.mark.parametrize("det_pitch", [0.05, 0.4, 3.0])
-def test_bp_smem_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch, algo):
+def test_bp_tile_rectangles_and_fallback(tk, oracle, monkeypatch, det_pitch, algo):
     """Fine detector pitch makes the CTA footprint exceed the shared-memory tile
     (global-gather fallback); coarse pitch makes whole volumes fit one tile."""
     monkeypatch.setenv("TK_BP_ALGO", algo)
@@ -657,18 +639,21 @@ def test_bp_tma_large_volume_edges(tk, oracle, monkeypatch, cols):
 
 def test_fp_fixed_row_stride_layout_matches_runtime_stride(tk, monkeypatch):
     """Large non-cubic volume: the compile-time row-stride cell layout (immediate-offset
-    far-row loads, used when the padding is < 2x) gives bit-identical projections to
-    the runtime-stride layout, views at 0/30/45/60/90 degrees."""
+    far-row loads, used when it wastes at most 2x the compact layout's memory) gives
+    bit-identical projections to the runtime-stride layout, views at 0/30/45/60/90
+    degrees, for the general and the mirror-pair kernel."""
     shape, sp = (520, 500, 510), (0.5, 0.5, 0.5)
     full = tk.circular_cone_geometry(shape, sp, (256, 300), (2.0, 2.0), 720, 2 * np.pi, 1200.0, 750.0)
     geom = tk.GeometryCone3D(shape, sp, (256, 300), (2.0, 2.0), [full.matrices[i] for i in (0, 60, 90, 120, 180)],
                              1200.0, 750.0)
     x = torch.rand(shape, device="cuda")
-    monkeypatch.setenv("TK_FPZ_NOFIX", "0")
-    a = tk.forward_project(tk.Volume(x, sp), geom).data
-    monkeypatch.setenv("TK_FPZ_NOFIX", "1")
-    b = tk.forward_project(tk.Volume(x, sp), geom).data
-    assert torch.equal(a, b) and float(a.abs().max()) > 0
+    for mirror in ("0", "1"):
+        monkeypatch.setenv("TK_FP_MIRROR", mirror)
+        monkeypatch.setenv("TK_FP_NOFIX", "0")
+        a = tk.forward_project(tk.Volume(x, sp), geom).data
+        monkeypatch.setenv("TK_FP_NOFIX", "1")
+        b = tk.forward_project(tk.Volume(x, sp), geom).data
+        assert torch.equal(a, b) and float(a.abs().max()) > 0
 
 
 def test_deterministic_cone_transpose(tk, oracle):
@@ -732,12 +717,11 @@ def test_nondeterministic_transposes_follow_torch_determinism(tk):
     bp_adjoint_tensor(x, geom)  # fine when the switch is off
 
 
-@pytest.mark.parametrize("knobs", [{"TK_FPZ_RB": "16"}, {"TK_FPZ_RB": "32"}, {"TK_FPZ_VG": "1"},
-                                   {"TK_FPZ_VG": "2"}, {"TK_FPZ_VG": "6"}, {"TK_FPZ_VG": "8"},
-                                   {"TK_FPZ_VG": "5"}, {"TK_FPZ_F2": "0"}, {"TK_FPZ_NOFIX": "1"}])
+@pytest.mark.parametrize("knobs", [{"TK_FP_CFG": "4x4"}, {"TK_FP_NOFIX": "1"},
+                                   {"TK_FP_MIRROR": "1"}, {"TK_FP_MIRROR": "1", "TK_FP_NOFIX": "1"},
+                                   {"TK_FP_MIRROR": "1", "TK_FP_CFG": "8x1"}, {"TK_FP_MIRROR": "1", "TK_FP_CFG": "8x2"}])
 def test_fp_tuning_knobs_keep_results(tk, monkeypatch, knobs):
-    """Every forward-projector tuning knob (CTA shape, views per CTA, pair layout,
-    fixed stride) must give the default's projection (same taps; bit-identical or
+    """Every forward-projector tuning knob (kernel, CTA shape, fixed stride) must give the default's projection (same taps; bit-identical or
     rounding-level), with no output element missed."""
     geom = tk.circular_cone_geometry((24, 28, 20), (0.9, 1.1, 1.0), (30, 34), (1.5, 1.4), 131, 2 * np.pi,
                                      1200.0, 750.0)
@@ -784,6 +768,7 @@ class TestMirrorForward:
         from paper_2511_08427_b200.projectors import forward_kernel_path
 
         geom = tk.circular_cone_geometry(shape, spacing, det, ds, views, 2 * np.pi, 1200.0, 750.0)
+        monkeypatch.setenv("TK_FP_MIRROR", "1")
         assert forward_kernel_path(geom) == "mirror"
         x = np.random.default_rng(7).standard_normal(shape).astype(np.float32).astype(np.float64)
         got = tk.forward_project(tk.Volume(x, spacing), geom).data
@@ -798,7 +783,8 @@ class TestMirrorForward:
 
     @pytest.mark.parametrize("cfg", ["4x3", "8x1", "8x2"])
     def test_launch_configurations(self, tk, oracle, monkeypatch, cfg):
-        monkeypatch.setenv("TK_FPM_CFG", cfg)
+        monkeypatch.setenv("TK_FP_MIRROR", "1")
+        monkeypatch.setenv("TK_FP_CFG", cfg)
         geom = tk.circular_cone_geometry((48,) * 3, (1.0,) * 3, (64, 80), (1.6, 1.6), 19, 2 * np.pi, 1200.0, 750.0)
         x = oracle.shepp_logan_3d((48,) * 3)
         got = tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data

@@ -254,9 +254,10 @@ class TestForwardKernelChoice:
     """tk_forward_cone_3d_path: the z-mirror-pair kernel runs exactly for
     z-mirror-symmetric scans whose volume fits its layout (host-only query)."""
 
-    def test_circular_orbits_use_the_mirror_kernel(self):
+    def test_circular_orbits_use_the_mirror_kernel(self, monkeypatch):
         from paper_2511_08427_b200.projectors import forward_kernel_path
 
+        monkeypatch.setenv("TK_FP_MIRROR", "1")
         for shape, det in [((512,) * 3, (1024, 1024)), ((256,) * 3, (512, 512)), ((33, 40, 21), (31, 45)),
                            ((16, 16, 16), (12, 12))]:
             g = tk.circular_cone_geometry(shape, (0.5,) * 3, det, (0.6, 0.6), 36, 2 * np.pi, 1200.0, 750.0)
@@ -265,6 +266,7 @@ class TestForwardKernelChoice:
     def test_other_scans_use_the_general_kernel(self, monkeypatch):
         from paper_2511_08427_b200.projectors import forward_kernel_path
 
+        monkeypatch.setenv("TK_FP_MIRROR", "1")
         det, ds = (64, 64), (1.6, 1.6)
         helix = tk.helical_trajectory_3d(36, 4 * np.pi, 1200.0, 750.0, det, ds, -20.0, 20.0)
         g = tk.GeometryCone3D((32,) * 3, (1,) * 3, det, ds, helix, 1200.0, 750.0)
@@ -278,8 +280,8 @@ class TestForwardKernelChoice:
         mats[:, 1, :] += 0.3 * mats[:, 2, :]
         g = tk.GeometryCone3D((32,) * 3, (1,) * 3, det, ds, [tk.ProjectionMatrix(m) for m in mats], 1200.0, 750.0)
         assert forward_kernel_path(g) == "general"
-        # too wide for the pair layout's compile-time row stride
-        g = tk.circular_cone_geometry((1024,) * 3, (0.25,) * 3, det, ds, 4, 2 * np.pi, 1200.0, 750.0)
+        # too large for 32-bit cell indices of the pair layout
+        g = tk.circular_cone_geometry((2048,) * 3, (0.125,) * 3, det, ds, 4, 2 * np.pi, 1200.0, 750.0)
         assert forward_kernel_path(g) == "general"
         monkeypatch.setenv("TK_FP_MIRROR", "0")
         assert forward_kernel_path(circ) == "general"
