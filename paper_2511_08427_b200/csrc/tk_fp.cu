@@ -35,7 +35,12 @@
 // segments, one launch per segment, to shrink the L2 working set of the
 // resident CTAs (DRAM reads 187 -> 52 GB for the mirror kernel, but +3.5 % time
 // per extra segment: the march is bound by L1 / L2 latency, not DRAM), and
-// staging each CTA's results in shared memory for full-segment writes (+1.6 %).
+// staging each CTA's results in shared memory for full-segment writes (+1.6 %);
+// a slab-staged variant (the CTA's bundle of rays marched slab by slab along its
+// major axis from shared-memory boxes filled by cp.async.bulk, bit-identical
+// results): 726 ms at 8-cell slabs, 654 ms with the copies disabled, ~410 ms
+// extrapolated to infinitely thick slabs -- the per-slab CTA-wide lockstep costs
+// more than the L1 misses it removes (git history: tk_fp.cu before 2026-10-17 16:00).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -398,8 +403,9 @@ using FpKern = void (*)(const float4 *, int, int, int, double, double, double, c
 static FpKern pick_kernel(bool mirror, bool fixs, int &vg) {
   const char *ce = getenv("TK_FP_CFG");
   const bool c8x1 = ce && !strcmp(ce, "8x1"), c8x2 = ce && !strcmp(ce, "8x2"), c4x4 = ce && !strcmp(ce, "4x4"),
-             c4x3 = ce && !strcmp(ce, "4x3");
+             c4x3 = ce && !strcmp(ce, "4x3"), c6x2 = ce && !strcmp(ce, "6x2");
   if (mirror) {
+    if (c6x2) return vg = 6, fixs ? cone_fp_mirror_kernel<6, 2, true> : cone_fp_mirror_kernel<6, 2, false>;
     if (c8x2) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 2, true> : cone_fp_mirror_kernel<8, 2, false>;
     if (c8x1) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 1, true> : cone_fp_mirror_kernel<8, 1, false>;
     return vg = 4, fixs ? cone_fp_mirror_kernel<4, 3, true> : cone_fp_mirror_kernel<4, 3, false>;

@@ -406,8 +406,8 @@ def _poison(shape):
     del t
 
 
-FP_KNOBS = [{}, {"TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x1", "TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "8x2", "TK_FP_MIRROR": "1"},
-            {"TK_FP_ALGO": "tex"}]
+FP_KNOBS = [{}, {"TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x1", "TK_FP_MIRROR": "1"},
+            {"TK_FP_CFG": "8x2", "TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "6x2", "TK_FP_MIRROR": "1"}, {"TK_FP_ALGO": "tex"}]
 
 
 @pytest.mark.parametrize("knobs", FP_KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
@@ -789,3 +789,4 @@ class TestMirrorForward:
         x = oracle.shepp_logan_3d((48,) * 3)
         got = tk.forward_project(tk.Volume(x, (1, 1, 1)), geom).data
         assert rel(got, oracle.forward_cone_3d(x, (1, 1, 1), geom.matrix_array(), (64, 80), 0.5)) < TOL
+
