@@ -53,7 +53,7 @@ NVOX = VOL[0] * VOL[1] * VOL[2]
 WORKLOAD = ("cfg4: cone-beam circular 512^3 @0.5 mm, 720 views over 2pi, 1024^2 detector @0.6 mm, "
             "sdd 1200 / sid 750: forward projection + FDK (shepp_logan) back-projection")
 METRIC = "cone-beam back/forward-projection GUPS at 512³×720 views, 1/2/4/8 B200 vs CPU"
-FP_KERNEL = "cone_fp4z_kernel"  # the default forward projector
+FP_KERNEL = "cone_fp_kernel"  # the default forward projector
 BP_KERNEL = "cone_bp_tma_kernel"  # the default back projector
 
 
@@ -226,7 +226,8 @@ def l1_peak():
 def ncu_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the newest committed full ncu
     capture of the cfg4 configuration (profiles/ncu_*.json)."""
-    for p in sorted((ROOT / "profiles").glob("ncu_*.json"), reverse=True):
+    caps = list((ROOT / "profiles").glob("ncu_*.json")) + list((ROOT / "profiles").glob("r*/ncu_*.json"))
+    for p in sorted(caps, key=lambda q: q.name, reverse=True):
         try:
             d = json.loads(p.read_text())
         except (ValueError, OSError):

@@ -43,6 +43,8 @@ _SIGS = {
     "ora_forward_fan_2d_transpose": [_D, _I, _I, _F, _F, _D, _D, _I, _F, _F, _I, _F, _F, _D],
     "ora_forward_cone_3d_transpose": [_D, _I, _I, _I, _F, _F, _F, _D, _D, _I, _I, _I, _F, _D],
     "ora_back_cone_3d_transpose": [_D, _I, _I, _I, _D, _F, _I, _I, _I, _I, _F, _F, _F, _D],
+    "ora_back_parallel_2d_transpose": [_D, _I, _I, _D, _D, _F, _I, _I, _F, _F, _D],
+    "ora_back_fan_2d_transpose": [_D, _I, _I, _D, _D, _F, _F, _F, _I, _I, _F, _F, _I, _D],
     "ora_num_threads": [],
     "ora_set_num_threads": [_I],
 }
@@ -286,6 +288,29 @@ def back_cone_3d_T(vol, mats, sid, detector_shape, spacing, weighted=False) -> n
     lib().ora_back_cone_3d_transpose(_p(vol), mats.shape[0], rows, cols, _p(mats), float(sid),
                                      int(bool(weighted)), nz, ny, nx, float(spacing[0]),
                                      float(spacing[1]), float(spacing[2]), _p(out))
+    return out
+
+
+def back_parallel_2d_T(img, angles, ds, n_det, spacing) -> np.ndarray:
+    """Exact transpose of back_parallel_2d (_kernels.py:174-195)."""
+    img = _f64(img)
+    ang = _f64(angles)
+    c, s = _f64(np.cos(ang)), _f64(np.sin(ang))
+    out = np.empty((ang.size, int(n_det)))
+    lib().ora_back_parallel_2d_transpose(_p(img), ang.size, int(n_det), _p(c), _p(s), float(ds), img.shape[0],
+                                         img.shape[1], float(spacing[0]), float(spacing[1]), _p(out))
+    return out
+
+
+def back_fan_2d_T(img, angles, sdd, sid, ds, n_det, spacing, weighted=False) -> np.ndarray:
+    """Exact transpose of back_fan_2d (_kernels.py:219-251)."""
+    img = _f64(img)
+    ang = _f64(angles)
+    c, s = _f64(np.cos(ang)), _f64(np.sin(ang))
+    out = np.empty((ang.size, int(n_det)))
+    lib().ora_back_fan_2d_transpose(_p(img), ang.size, int(n_det), _p(c), _p(s), float(sdd), float(sid),
+                                    float(ds), img.shape[0], img.shape[1], float(spacing[0]), float(spacing[1]),
+                                    int(bool(weighted)), _p(out))
     return out
 
 

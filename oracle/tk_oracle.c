@@ -464,3 +464,57 @@ void ora_back_cone_3d_transpose(const double *vol, int n_views, int rows, int co
     }
   }
 }
+
+/* Exact transposes of the 2D voxel-driven back projectors (back_parallel_2d,
+ * _kernels.py:174-195; back_fan_2d, :219-251): every pixel scatters its value
+ * times the two linear-interpolation weights it gathers with (and the fan
+ * distance weight) into the sinogram row of each angle.  Angles are
+ * independent rows: parallel over angles, deterministic. */
+void ora_back_parallel_2d_transpose(const double *img, int n_ang, int n_det, const double *cos_a,
+                                    const double *sin_a, double ds, int ny, int nx, double sy,
+                                    double sx, double *sino) {
+  double half = (n_det - 1) / 2.0;
+  double cy = (ny - 1) / 2.0, cx = (nx - 1) / 2.0;
+#pragma omp parallel for schedule(static)
+  for (int ia = 0; ia < n_ang; ++ia) {
+    double *row = sino + (long)ia * n_det;
+    for (int j = 0; j < n_det; ++j) row[j] = 0.0;
+    for (long idx = 0; idx < (long)ny * nx; ++idx) {
+      long iy = idx / nx, ix = idx % nx;
+      double x = (ix - cx) * sx, y = (iy - cy) * sy;
+      double f = (x * cos_a[ia] + y * sin_a[ia]) / ds + half;
+      long j0 = (long)floor(f);
+      double w = f - j0, g = img[idx];
+      if (0 <= j0 && j0 < n_det) row[j0] += (1.0 - w) * g;
+      if (0 <= j0 + 1 && j0 + 1 < n_det) row[j0 + 1] += w * g;
+    }
+  }
+}
+
+void ora_back_fan_2d_transpose(const double *img, int n_ang, int n_det, const double *cos_a,
+                               const double *sin_a, double sdd, double sid, double ds, int ny,
+                               int nx, double sy, double sx, int weighted, double *sino) {
+  double half = (n_det - 1) / 2.0;
+  double cy = (ny - 1) / 2.0, cx = (nx - 1) / 2.0;
+#pragma omp parallel for schedule(static)
+  for (int ia = 0; ia < n_ang; ++ia) {
+    double *row = sino + (long)ia * n_det;
+    double ct = cos_a[ia], st = sin_a[ia];
+    for (int j = 0; j < n_det; ++j) row[j] = 0.0;
+    for (long idx = 0; idx < (long)ny * nx; ++idx) {
+      long iy = idx / nx, ix = idx % nx;
+      double x = (ix - cx) * sx, y = (iy - cy) * sy;
+      double w = sid - x * ct - y * st;
+      if (w <= TINY) continue;
+      double f = sdd * (-x * st + y * ct) / w / ds + half;
+      long j0 = (long)floor(f);
+      double fw = f - j0, g = img[idx];
+      if (weighted) {
+        double q = sid / w;
+        g *= q * q;
+      }
+      if (0 <= j0 && j0 < n_det) row[j0] += (1.0 - fw) * g;
+      if (0 <= j0 + 1 && j0 + 1 < n_det) row[j0 + 1] += fw * g;
+    }
+  }
+}
