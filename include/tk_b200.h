@@ -154,6 +154,17 @@ int tk_forward_fan_2d_adjoint(const float *sino, int n_ang, int n_det,
                               double sdd, double sid, double ds, double step,
                               int ny, int nx, double sy, double sx, float *vol_out,
                               void *stream);
+/* Exact transposes B^T of tk_back_parallel_2d / tk_back_fan_2d (the matched adjoint
+ * of the reference's voxel-driven 2D back projectors, _kernels.py:174-251; the
+ * reference's own VJP of back projection is the paired A, autodiff.py:65-68).
+ * sino_out (n_ang, n_det) is overwritten; weighted = 1 applies (sid / w)^2 (fan). */
+int tk_back_parallel_2d_adjoint(const float *img, int ny, int nx, double sy, double sx,
+                                const double *cos_a, const double *sin_a, int n_ang,
+                                int n_det, double ds, float *sino_out, void *stream);
+int tk_back_fan_2d_adjoint(const float *img, int ny, int nx, double sy, double sx,
+                           const double *cos_a, const double *sin_a, int n_ang, double sdd,
+                           double sid, int n_det, double ds, int weighted, float *sino_out,
+                           void *stream);
 
 /* ---- FFT row filter (filters.py:136-171, 204-211) ---------------------------
  * For each of n_rows rows of `width` samples (row r belongs to detector row

@@ -62,6 +62,10 @@ SIGNATURES = {
                                        _c_int, _c_dbl, _c_dbl, _ptr, _ptr],
     "tk_forward_fan_2d_adjoint": [_ptr, _c_int, _c_int, _dptr, _dptr, _c_dbl, _c_dbl, _c_dbl,
                                   _c_dbl, _c_int, _c_int, _c_dbl, _c_dbl, _ptr, _ptr],
+    "tk_back_parallel_2d_adjoint": [_ptr, _c_int, _c_int, _c_dbl, _c_dbl, _dptr, _dptr, _c_int, _c_int, _c_dbl,
+                                    _ptr, _ptr],
+    "tk_back_fan_2d_adjoint": [_ptr, _c_int, _c_int, _c_dbl, _c_dbl, _dptr, _dptr, _c_int, _c_dbl, _c_dbl, _c_int,
+                               _c_dbl, _c_int, _ptr, _ptr],
     "tk_fft_filter_rows": [_ptr, _c_ll, _c_int, _c_int, _dptr, _c_int, _c_dbl, _c_dbl, _c_dbl,
                            _c_dbl, _ptr, _ptr],
     "tk_fft_filter_rows_ex": [_ptr, _c_ll, _c_int, _c_int, _c_int, _c_int, _dptr, _c_int, _c_dbl,

@@ -202,6 +202,57 @@ __global__ void __launch_bounds__(256)
   if (active) out[(long long)iy * nx + ix] = acc;
 }
 
+// Exact transposes B^T of the voxel-driven gathers above: one CTA per angle;
+// every pixel scatters its value times the two interpolation weights it gathers
+// with (times the fan distance weight) into the angle's detector row, accumulated
+// with shared-memory atomics (rows up to kBt2Max detectors) or global atomics.
+// fp32 atomics: summation order is not deterministic.
+constexpr int kBt2Max = 12288;
+template <bool FAN, bool WEIGHTED, bool SMEM>
+__global__ void __launch_bounds__(256)
+    bp2d_adjoint_kernel(const float *__restrict__ img, int n_det, const Bp2View *__restrict__ views, float half,
+                        float sdd_over_ds, float sid, int nx, int ny, float sx, float sy,
+                        float *__restrict__ sino) {
+  extern __shared__ float row_acc[];
+  const int a = blockIdx.x;
+  const Bp2View V = views[a];
+  float *row = SMEM ? row_acc : sino + (long long)a * n_det;
+  if (SMEM) {
+    for (int j = threadIdx.x; j < n_det; j += blockDim.x) row[j] = 0.f;
+    __syncthreads();
+  }
+  const long long npix = (long long)nx * ny;
+  for (long long i = threadIdx.x; i < npix; i += blockDim.x) {
+    const float g = __ldg(img + i);
+    if (g == 0.f) continue;
+    const int ix = (int)(i % nx), iy = (int)(i / nx);
+    const float x = ((float)ix - (nx - 1) * 0.5f) * sx;
+    const float y = ((float)iy - (ny - 1) * 0.5f) * sy;
+    float f, q = 1.f;
+    if (!FAN) {
+      f = fmaf(x, V.c, fmaf(y, V.s, half));
+    } else {
+      const float w = sid - x * V.c - y * V.s;
+      if (!(w > 1e-12f)) continue;
+      const float rw = 1.f / w;
+      f = fmaf(sdd_over_ds * (y * V.c - x * V.s), rw, half);
+      if (WEIGHTED) {
+        q = sid * rw;
+        q *= q;
+      }
+    }
+    const float fl = floorf(f);
+    const int j0 = (int)fl;
+    const float w = f - fl, gq = g * q;
+    if ((unsigned)j0 < (unsigned)n_det) atomicAdd(row + j0, (1.f - w) * gq);
+    if ((unsigned)(j0 + 1) < (unsigned)n_det) atomicAdd(row + j0 + 1, w * gq);
+  }
+  if (SMEM) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < n_det; j += blockDim.x) sino[(long long)a * n_det + j] = row[j];
+  }
+}
+
 static int upload_angles(Scratch &d, const double *cos_a, const double *sin_a, int n,
                          cudaStream_t st) {
   std::vector<double2> h(n);
@@ -271,11 +322,54 @@ static int bp2d(bool fan, const float *sino, int n_ang, int n_det, const double 
   return TK_OK;
 }
 
+static int bp2d_adjoint(bool fan, const float *img, int ny, int nx, double sy, double sx, const double *cos_a,
+                        const double *sin_a, int n_ang, double sdd, double sid, int n_det, double ds, bool weighted,
+                        float *sino, void *stream) {
+  clear_error();
+  if (!img || !sino || !cos_a || !sin_a) return fail_arg("2D back-projection transpose: null pointer");
+  if (ny < 1 || nx < 1 || n_ang < 1 || n_det < 1) return fail_arg("2D back-projection transpose: non-positive extent");
+  if (!(sx > 0 && sy > 0 && ds > 0)) return fail_arg("2D back-projection transpose: spacing must be > 0");
+  if (fan && !(sid > 0 && sid < sdd)) return fail_arg("fan back projector requires 0 < sid < sdd");
+  if (!fan && weighted) return fail_arg("parallel backprojection has no distance weighting");
+  cudaStream_t st = as_stream(stream);
+  std::vector<Bp2View> h(n_ang);
+  for (int i = 0; i < n_ang; ++i) {
+    h[i].c = (float)(fan ? cos_a[i] : cos_a[i] / ds);
+    h[i].s = (float)(fan ? sin_a[i] : sin_a[i] / ds);
+  }
+  Scratch d;
+  TK_TRY_CUDA(upload(d, h.data(), sizeof(Bp2View) * n_ang, st));
+  const float half = (float)((n_det - 1) / 2.0), sdd_ds = (float)(sdd / ds);
+  const bool smem = n_det <= kBt2Max;
+  const size_t sb = smem ? sizeof(float) * n_det : 0;
+  if (!smem) TK_TRY_CUDA(cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)n_ang * n_det, st));
+  auto kern = fan ? (weighted ? (smem ? bp2d_adjoint_kernel<true, true, true> : bp2d_adjoint_kernel<true, true, false>)
+                              : (smem ? bp2d_adjoint_kernel<true, false, true> : bp2d_adjoint_kernel<true, false, false>))
+                  : (smem ? bp2d_adjoint_kernel<false, false, true> : bp2d_adjoint_kernel<false, false, false>);
+  if (sb > 48 * 1024) TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  kern<<<n_ang, 256, sb, st>>>(img, n_det, d.as<Bp2View>(), half, sdd_ds, (float)sid, nx, ny, (float)sx, (float)sy,
+                               sino);
+  TK_LAUNCHED("bp2d_adjoint_kernel");
+  return TK_OK;
+}
+
 }  // namespace tk
 
 using namespace tk;
 
 extern "C" {
+
+int tk_back_parallel_2d_adjoint(const float *img, int ny, int nx, double sy, double sx, const double *cos_a,
+                                const double *sin_a, int n_ang, int n_det, double ds, float *sino_out, void *stream) {
+  return bp2d_adjoint(false, img, ny, nx, sy, sx, cos_a, sin_a, n_ang, 0.0, 0.0, n_det, ds, false, sino_out, stream);
+}
+
+int tk_back_fan_2d_adjoint(const float *img, int ny, int nx, double sy, double sx, const double *cos_a,
+                           const double *sin_a, int n_ang, double sdd, double sid, int n_det, double ds, int weighted,
+                           float *sino_out, void *stream) {
+  return bp2d_adjoint(true, img, ny, nx, sy, sx, cos_a, sin_a, n_ang, sdd, sid, n_det, ds, weighted != 0, sino_out,
+                      stream);
+}
 
 int tk_forward_parallel_2d(const float *vol, int ny, int nx, double sy, double sx,
                            const double *cos_a, const double *sin_a, int n_ang, int n_det,

@@ -126,9 +126,6 @@ class _BackProjection(torch.autograd.Function):
     def backward(ctx, grad):
         grad = grad.contiguous().float()
         if ctx.adjoint == "matched":
-            if not isinstance(ctx.geometry, GeometryCone3D):
-                raise NotImplementedError("exact B^T is implemented for cone geometry; use "
-                                          "adjoint='paired' for 2D back projection")
             g = _backproject_T(grad, ctx.geometry, ctx.weighted)
         else:
             if ctx.weighted:

@@ -299,23 +299,38 @@ def _alert_nondeterministic(what: str) -> None:
             raise RuntimeError(msg)
 
 
-def bp_adjoint_tensor(vol: torch.Tensor, geom: GeometryCone3D, weighted: bool = False) -> torch.Tensor:
-    """Exact transpose B^T of the voxel-driven cone back projector (fp32 atomics:
-    summation order not deterministic; raises under torch deterministic mode)."""
-    if not isinstance(geom, GeometryCone3D):
-        raise TypeError("the exact back-projection transpose is implemented for cone geometry")
-    _alert_nondeterministic("the cone back-projection transpose")
+def bp_adjoint_tensor(vol: torch.Tensor, geom, weighted: bool = False) -> torch.Tensor:
+    """Exact transpose B^T of the voxel-driven back projector, cone or 2D (fp32
+    atomics: summation order not deterministic; raises under torch deterministic mode)."""
+    what = "cone" if isinstance(geom, GeometryCone3D) else "2D"
+    _alert_nondeterministic(f"the {what} back-projection transpose")
     vol = _prep(vol, geom.volume_shape, "volume")
     with torch.cuda.device(vol.device):
         out = _new(geom.sinogram_shape, vol)
-        mats, pm = _lib.host_f64(geom.matrix_array())
-        nz, ny, nx = geom.volume_shape
-        sz, sy, sx = geom.volume_spacing
-        rows, cols = geom.detector_shape
-        _lib.call("tk_back_cone_3d_adjoint", _lib.dev_ptr(vol), nz, ny, nx, sz, sy, sx, pm, geom.sid,
-                  int(bool(weighted)), geom.n_projections, rows, cols, _lib.dev_ptr(out),
-                  _lib.stream_ptr(vol.device))
-    return out
+        s = _lib.stream_ptr(vol.device)
+        if isinstance(geom, GeometryCone3D):
+            mats, pm = _lib.host_f64(geom.matrix_array())
+            nz, ny, nx = geom.volume_shape
+            sz, sy, sx = geom.volume_spacing
+            rows, cols = geom.detector_shape
+            _lib.call("tk_back_cone_3d_adjoint", _lib.dev_ptr(vol), nz, ny, nx, sz, sy, sx, pm, geom.sid,
+                      int(bool(weighted)), geom.n_projections, rows, cols, _lib.dev_ptr(out), s)
+            return out
+        if isinstance(geom, GeometryParallel2D):
+            (c, pc), (sn, ps) = (_lib.host_f64(a) for a in geom.trig)
+            ny, nx = geom.volume_shape
+            sy, sx = geom.volume_spacing
+            if isinstance(geom, GeometryFan2D):
+                _lib.call("tk_back_fan_2d_adjoint", _lib.dev_ptr(vol), ny, nx, sy, sx, pc, ps, geom.n_projections,
+                          geom.sdd, geom.sid, geom.detector_width, geom.detector_spacing, int(bool(weighted)),
+                          _lib.dev_ptr(out), s)
+            else:
+                if weighted:
+                    raise ValueError("parallel backprojection has no distance weighting")
+                _lib.call("tk_back_parallel_2d_adjoint", _lib.dev_ptr(vol), ny, nx, sy, sx, pc, ps,
+                          geom.n_projections, geom.detector_width, geom.detector_spacing, _lib.dev_ptr(out), s)
+            return out
+    raise TypeError(f"unsupported geometry {type(geom).__name__}")
 
 
 # ---------------------------------------------------------------------------
@@ -418,10 +433,11 @@ def transpose_forward_project(sino: Sinogram, geom, cfg: SamplingConfig = _DEFAU
     return Volume(fp_adjoint_tensor(sino.data, geom, cfg.step(geom.volume_spacing)), geom.volume_spacing)
 
 
-def transpose_back_project(vol: Volume, geom: GeometryCone3D, fdk_weighting: bool = False) -> Sinogram:
-    """Exact B^T (matched adjoint of the voxel-driven cone back projector)."""
-    _check_volume(vol, geom, 3)
-    return Sinogram(bp_adjoint_tensor(vol.data, geom, fdk_weighting), geom.detector_spacing)
+def transpose_back_project(vol: Volume, geom, fdk_weighting: bool = False) -> Sinogram:
+    """Exact B^T (matched adjoint of the voxel-driven back projector: cone, fan or parallel)."""
+    _check_volume(vol, geom, 3 if isinstance(geom, GeometryCone3D) else 2)
+    spacing = geom.detector_spacing if isinstance(geom, GeometryCone3D) else (geom.detector_spacing,)
+    return Sinogram(bp_adjoint_tensor(vol.data, geom, fdk_weighting), spacing)
 
 
 def _sizes(geom):

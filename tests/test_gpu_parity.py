@@ -453,6 +453,36 @@ def test_fp_transpose_matches_oracle(tk, oracle):
         assert rel(got, want) < TOL
 
 
+def test_2d_bp_transpose_matches_oracle(tk, oracle):
+    """Exact B^T of the 2D voxel-driven back projectors (parallel; fan with and without
+    the distance weight) against the oracle's transposes, plus the matched dot test
+    and the autograd path BackProjection(adjoint='matched')."""
+    rng = np.random.default_rng(41)
+    ang = tk.circular_trajectory_2d(53, np.pi)
+    gp = tk.GeometryParallel2D((37, 41), (0.9, 1.1), 59, 1.3, ang)
+    x = rng.standard_normal((37, 41))
+    got = tk.transpose_back_project(tk.Volume(x, (0.9, 1.1)), gp).data
+    assert rel(got, oracle.back_parallel_2d_T(x, ang, 1.3, 59, (0.9, 1.1))) < TOL
+    angf = tk.circular_trajectory_2d(61, 2 * np.pi)
+    gf = tk.GeometryFan2D((37, 41), (0.9, 1.1), 70, 1.6, angf, sdd=1200.0, sid=750.0)
+    for w in (False, True):
+        got = tk.transpose_back_project(tk.Volume(x, (0.9, 1.1)), gf, w).data
+        assert rel(got, oracle.back_fan_2d_T(x, angf, 1200.0, 750.0, 1.6, 70, (0.9, 1.1), w)) < TOL
+    for g in (gp, gf):
+        assert tk.dot_test(tk.back_projection_op(g, matched=True), trials=3) <= 1e-4
+    # wide detector: global-atomic path (rows longer than the shared-memory row buffer)
+    gw = tk.GeometryParallel2D((24, 24), (1.0, 1.0), 13000, 0.01, ang[:5])
+    xw = rng.standard_normal((24, 24))
+    got = tk.transpose_back_project(tk.Volume(xw, (1.0, 1.0)), gw).data
+    assert rel(got, oracle.back_parallel_2d_T(xw, ang[:5], 0.01, 13000, (1.0, 1.0))) < TOL
+    y = torch.tensor(rng.standard_normal((61, 70)), dtype=torch.float32, device="cuda", requires_grad=True)
+    out = tk.FanBackProjection2D.apply(y, gf, "matched", True)
+    gx = torch.randn_like(out)
+    out.backward(gx)
+    want = tk.transpose_back_project(tk.Volume(gx, (0.9, 1.1)), gf, True).data
+    assert rel(y.grad, want.cpu().numpy()) < 1e-6
+
+
 def test_bp_transpose_matches_oracle(tk, oracle):
     shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
     hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
