@@ -272,6 +272,72 @@ __global__ void __launch_bounds__(128 * VG, CPS)
   if (rm != r) *dstm = a.y * fs;
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative march (TK_FP_ALGO=warp): the north star's formulation, kept
+// as the measured comparison.  A warp walks ONE ray at a time: lane l takes the
+// samples base + l of every 32-sample stride (same sample positions, cells and
+// arithmetic as cone_fp_kernel) and the 32 partial sums are combined with a
+// __shfl_xor_sync tree.  Each lane's consecutive samples are 32 apart, so no
+// lane reuses a cell, and the 32 lanes' cells lie along the ray (a new line per
+// x / y crossing) instead of across the quarter-warp's z-contiguous cells:
+// every sample loads, ~16 lines per warp load.  CTA = the 16 x 8 detector tile
+// of one view; lane i of warp w sets up ray i of the warp's 4-column x 8-row
+// sub-tile (float64), then broadcasts it to the warp.
+// ---------------------------------------------------------------------------
+template <bool FIXS>
+__global__ void __launch_bounds__(128)
+    cone_fp_warp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
+                        const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
+                        float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+  const int ncb = (cols + kFpCols - 1) / kFpCols;
+  const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
+  const int v = (int)(bt % n_views), rb = (int)(bt / n_views);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = cb * kFpCols + warp * 4 + (lane >> 3), r = rb * kFpRows + (lane & 7);
+  const bool valid = c < cols && r < rows;
+  RaySetup rs;
+  const bool live = valid && cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs);
+  const float magic = 8388608.f;
+  const unsigned sys = FIXS ? kFpFixS : ystride;
+  const unsigned long long m2 = pk2(magic, magic);
+  float mine = 0.f;
+  for (int i = 0; i < 32; ++i) {
+    const int n = __shfl_sync(0xffffffffu, live ? rs.n : 0, i);
+    if (n == 0) continue;  // warp-uniform
+    const float ex = __shfl_sync(0xffffffffu, rs.ex, i) + (kFpMargin - 1);
+    const float ey = __shfl_sync(0xffffffffu, rs.ey, i) + (kFpMargin - 1);
+    const float ez = __shfl_sync(0xffffffffu, rs.ez, i) + (kFpMargin - 1);
+    const float gx = __shfl_sync(0xffffffffu, rs.gx, i), gy = __shfl_sync(0xffffffffu, rs.gy, i);
+    const float gz = __shfl_sync(0xffffffffu, rs.gz, i), last = __shfl_sync(0xffffffffu, rs.last, i);
+    const unsigned long long e2 = pk2(ex, ey), g2 = pk2(gx, gy);
+    float acc = 0.f;
+    for (int k = lane; k < n; k += 32) {
+      const float kk = k < n - 1 ? (float)k + 0.5f : (float)(n - 1) + 0.5f * last;
+      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
+      const float fz = fmaf(kk, gz, ez);
+      const unsigned long long xxy = fadd2_rm(fxy, m2);
+      const float xz = __fadd_rd(fz, magic);
+      const float2 xb = upk2(xxy);
+      const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
+      const float4 *p = elem_ptr(q, id);
+      const float4 lo4 = __ldg(p), hi4 = __ldg(p + sys);
+      const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
+      const float wz = fz - (xz - magic);
+      const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
+      const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
+      const float sv = lerpf(fmaf(wz, tl.y, tl.x), fmaf(wz, th.y, th.x), w.y);
+      acc = k < n - 1 ? acc + sv : fmaf(last, sv, acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == i) mine = acc * (float)step;
+  }
+  if (valid) out[((long long)v * rows + r) * cols + c] = live ? mine : 0.f;
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -309,7 +375,7 @@ static int env_int(const char *name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
-static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L) {
+static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L, bool force_runtime_stride = false) {
   constexpr int m2 = 2 * kFpMargin;
   L = FpLayout();
   L.mirror = mirror;
@@ -321,7 +387,7 @@ static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L) {
   const unsigned long long compact = rows * xc * zc;
   const unsigned fixs = mirror ? kMirS : kFpFixS, zres = mirror ? 5u : 255u;
   const unsigned zpf = zc + (zres + 256u - zc % 256u) % 256u;
-  const bool nofix = env_int("TK_FP_NOFIX", 0) != 0;  // 1: always the runtime stride (tests)
+  const bool nofix = force_runtime_stride || env_int("TK_FP_NOFIX", 0) != 0;  // 1: always the runtime stride (tests)
   if (!nofix && (unsigned long long)xc * zpf <= fixs && rows * fixs <= 2 * compact && rows * fixs < (1ull << 32)) {
     L.fixs = true;
     L.zpitch = zpf;
@@ -371,8 +437,18 @@ static int plan_cells(FpPlan &pl, bool mirror, cudaStream_t st) {
   FpLayout &L = pl.lay[k];
   if (!make_layout(pl.nz, pl.ny, pl.nx, mirror, L))
     return fail_arg("tk_forward_cone_3d: volume too large for 32-bit cell indices");
-  const size_t bytes = L.cell_bytes * (size_t)(pl.ny + 2 * kFpMargin) * L.ystride;
-  TK_TRY_CUDA(cudaMallocAsync(&pl.cells[k], bytes, st));
+  size_t bytes = L.cell_bytes * (size_t)(pl.ny + 2 * kFpMargin) * L.ystride;
+  cudaError_t e = cudaMallocAsync(&pl.cells[k], bytes, st);
+  if (e == cudaErrorMemoryAllocation && L.fixs) {  // the fixed stride pads: retry with the compact layout
+    (void)cudaGetLastError();
+    make_layout(pl.nz, pl.ny, pl.nx, mirror, L, true);
+    bytes = L.cell_bytes * (size_t)(pl.ny + 2 * kFpMargin) * L.ystride;
+    e = cudaMallocAsync(&pl.cells[k], bytes, st);
+  }
+  if (e != cudaSuccess) {
+    pl.cells[k] = nullptr;
+    return check_cuda(e, "cudaMallocAsync (forward-projection cells)");
+  }
   if (mirror) {
     dim3 g(ceil_div(L.zcells, 32), ceil_div(pl.nx + 2 * kFpMargin, 32), pl.ny + 2 * kFpMargin);
     fp_mirror_cells_kernel<<<g, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, static_cast<float4 *>(pl.cells[k]),
@@ -427,6 +503,17 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
   }
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
+  const char *algo = getenv("TK_FP_ALGO");
+  if (!mirror && algo && !strcmp(algo, "warp")) {  // warp-cooperative comparison kernel
+    const long long nbw = (long long)ceil_div(cols, kFpCols) * ceil_div(rows, kFpRows) * n_views;
+    if (nbw >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
+    auto kw = L.fixs ? cone_fp_warp_kernel<true> : cone_fp_warp_kernel<false>;
+    kw<<<(unsigned)nbw, 128, 0, st>>>(static_cast<const float4 *>(pl.cells[0]), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
+                                      pl.sz, dviews.as<ConeRayView>(), rows, cols, n_views, step, out, L.zpitch,
+                                      L.ystride);
+    TK_LAUNCHED("cone_fp_warp_kernel");
+    return TK_OK;
+  }
   int vg = 1;
   FpKern kern = pick_kernel(mirror, L.fixs, vg);
   const int brows = mirror ? (rows + 1) / 2 : rows;
@@ -457,7 +544,8 @@ using namespace tk;
 
 extern "C" {
 
-// TK_FP_ALGO = default (tk_fp.cu) | tex | hwtex (texture-unit comparison, tk_fp_tex.cu)
+// TK_FP_ALGO = default (tk_fp.cu) | warp (warp-cooperative comparison, tk_fp.cu) | tex | hwtex
+// (texture-unit comparison, tk_fp_tex.cu)
 int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                        const double *sources, const double *minv, int n_views, int rows, int cols, double step,
                        float *out, void *stream) {

@@ -407,7 +407,8 @@ def _poison(shape):
 
 
 FP_KNOBS = [{}, {"TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x1", "TK_FP_MIRROR": "1"},
-            {"TK_FP_CFG": "8x2", "TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "6x2", "TK_FP_MIRROR": "1"}, {"TK_FP_ALGO": "tex"}]
+            {"TK_FP_CFG": "8x2", "TK_FP_MIRROR": "1"}, {"TK_FP_CFG": "6x2", "TK_FP_MIRROR": "1"}, {"TK_FP_ALGO": "tex"},
+            {"TK_FP_ALGO": "warp"}]
 
 
 @pytest.mark.parametrize("knobs", FP_KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
