@@ -44,19 +44,36 @@ struct BtMeta {
   int c0, r0, fits, pad;
 };
 
-// ZB z-voxels per thread (16 or 32: 32 halves the per-view set-up per update),
-// NST stages in the mbarrier ring.
-template <bool WEIGHTED, int ZB, int NST>
+// ZB = 32 z-voxels per thread (halves the per-view set-up per update against 16);
+// BW = the tile row pitch (floats) = the TMA box width, a compile-time constant so a
+// voxel's two tile rows are ONE IMAD (row bits x 4 BW + per-view base) and four LDS
+// with immediate offsets (0, 4, 4 BW, 4 BW + 4); nst (<= kBtMaxStages) stages in the
+// mbarrier ring.
+__device__ __forceinline__ float lds_at(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ float lds_off(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+
+template <int BW>
 __global__ void __launch_bounds__(kBtThreads, 2)
-    cone_bp_tma_kernel(const __grid_constant__ CUtensorMap map, const BpParams p, int bw, int bh,
-                       int stage_floats) {
-  constexpr int kBtZB = ZB, kBtStages = NST;
+    cone_bp_tma_kernel(const __grid_constant__ CUtensorMap map, const BpParams p, int weighted, int bh,
+                       int stage_floats, int nst, unsigned fbias) {
+  constexpr int kBtZB = 32, bw = BW;
+  const int kBtStages = nst;
   extern __shared__ float bt_raw[];  // [kBtStages][stage_floats] at a 128-byte aligned base
   // align by an element offset (not through uintptr_t) so the compiler keeps
   // the pointer in the shared window: LDS with 32-bit addresses, not generic LD
   float *bt_tiles = bt_raw + (((128u - (smem_u32(bt_raw) & 127u)) & 127u) >> 2);
-  __shared__ __align__(8) uint64_t full[kBtStages], empty[kBtStages];
-  __shared__ BtMeta meta[kBtStages];
+  const unsigned tiles_u32 = smem_u32(bt_tiles);
+  __shared__ __align__(8) uint64_t full[kBtMaxStages], empty[kBtMaxStages];
+  __shared__ BtMeta meta[kBtMaxStages];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -78,9 +95,11 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     const float bz0 = (float)(p.z_begin + zl0) - p.cz;
     const float bz1 = bz0 + (float)(kBtZB - 1);  // consumers evaluate all kBtZB rows (stores are masked)
     const unsigned tx_bytes = (unsigned)(bw * bh * 4);
-    for (int v = 0; v < p.n_views; ++v) {
-      const int s = v % kBtStages;
-      if (v >= kBtStages) mbar_wait(&empty[s], (unsigned)((v / kBtStages - 1) & 1));
+    int s = 0;
+    unsigned eph = 1u;  // parity of the empty-barrier phase to wait for (the first lap does not wait)
+    for (int v = 0; v < p.n_views; ++v, ++s) {
+      if (s == kBtStages) s = 0, eph ^= 1u;
+      if (v >= kBtStages) mbar_wait(&empty[s], eph);
       const ConeVoxView &V = p.views[v];
       float cmin = 3e38f, cmax = -3e38f, rmin = 3e38f, rmax = -3e38f;
       bool behind = false;
@@ -151,9 +170,11 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     accp[k >> 1] = pk2(a.x, a.y);
   };
 
-  for (int v = 0; v < p.n_views; ++v) {
-    const int s = v % kBtStages;
-    mbar_wait(&full[s], (unsigned)((v / kBtStages) & 1));
+  int s = 0;
+  unsigned fph = 0u;
+  for (int v = 0; v < p.n_views; ++v, ++s) {
+    if (s == kBtStages) s = 0, fph ^= 1u;
+    mbar_wait(&full[s], fph);
     const BtMeta m = meta[s];
     const ConeVoxView &V = p.views[v];  // uniform across the CTA: L1 broadcast (measured faster than a smem copy)
     const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
@@ -166,7 +187,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
       const float xcf = floor_magic(fc);
       const float wc = fc - (xcf - kFloorMagic);
       float q = 1.f;
-      if (WEIGHTED) {  // (sid / w)^2, _kernels.py:318-320
+      if (weighted) {  // (sid / w)^2, _kernels.py:318-320 (uniform branch)
         q = p.sid * rw;
         q *= q;
       }
@@ -174,9 +195,12 @@ __global__ void __launch_bounds__(kBtThreads, 2)
       const float fr0 = fmaf(b0, rw, p.cv);
       const float dr = V.b[2] * rw;
       if (m.fits) {
-        const float *t = bt_tiles + (size_t)s * stage_floats +
-                         ((int)(__float_as_uint(xcf) - kFloorBits) - m.c0);
-        const int rbias = (int)kFloorBits + m.r0;
+        // byte address of tap (row bits, c0) = row_bits * 4 BW + vbase (mod 2^32): the
+        // FADD.RM floor's float bits ARE kFloorBits + row
+        // fbias = 4 kFloorBits (BW + 1) (mod 2^32) arrives as a kernel argument: as a literal
+        // the compiler splits it off the base and re-adds it before every LDS (4 IADD per voxel)
+        const unsigned vbase = tiles_u32 + 4u * (unsigned)(s * stage_floats) +
+                               4u * (__float_as_uint(xcf) - (unsigned)m.c0) - (unsigned)m.r0 * (4u * BW) - fbias;
         const unsigned long long drp = pk2(dr, dr), fr0p = pk2(fr0, fr0), g0p = pk2(g0, g0), g1p = pk2(g1, g1);
         const unsigned long long mg = pk2(kFloorMagic, kFloorMagic);
 #pragma unroll
@@ -184,10 +208,11 @@ __global__ void __launch_bounds__(kBtThreads, 2)
           const unsigned long long frp = ffma2(pk2((float)(2 * j), (float)(2 * j + 1)), drp, fr0p);
           const unsigned long long xrp = fadd2_rm(frp, mg);  // floor_magic of both rows
           const float2 xr = upk2(xrp);
-          const float *ea = t + ((int)__float_as_uint(xr.x) - rbias) * bw;
-          const float *eb = t + ((int)__float_as_uint(xr.y) - rbias) * bw;
-          const unsigned long long e0 = pk2(ea[0], eb[0]), e1 = pk2(ea[1], eb[1]);
-          const unsigned long long e2 = pk2(ea[bw], eb[bw]), e3 = pk2(ea[bw + 1], eb[bw + 1]);
+          const unsigned ea = __float_as_uint(xr.x) * (4u * BW) + vbase;
+          const unsigned eb = __float_as_uint(xr.y) * (4u * BW) + vbase;
+          const unsigned long long e0 = pk2(lds_at(ea), lds_at(eb)), e1 = pk2(lds_off<4>(ea), lds_off<4>(eb));
+          const unsigned long long e2 = pk2(lds_off<4 * BW>(ea), lds_off<4 * BW>(eb));
+          const unsigned long long e3 = pk2(lds_off<4 * BW + 4>(ea), lds_off<4 * BW + 4>(eb));
           const unsigned long long top = ffma2(g1p, e1, fmul2(g0p, e0));
           const unsigned long long bot = ffma2(g1p, e3, fmul2(g0p, e2));
           const unsigned long long frac = fsub2(frp, fsub2(xrp, mg));
@@ -292,41 +317,45 @@ static void footprint_box(const BpParams &p, const ConeVoxView *hv, int kBtZB, i
         }
   }
   bw = ((wmax + 3 + 2 + 3) / 4) * 4;  // +3 for the 16-byte aligned start column, +2 slack
-  // row pitch == 12 or 20 (mod 32): adjacent tile rows shift by 12 / 20 banks, so
-  // an 8 x 4 warp's taps on neighbouring rows do not collide (bp_bank_model.py)
-  while (bw % 32 != 12 && bw % 32 != 20) bw += 4;
   bh = hmax + 2;
 }
 
-template <int ZB, int NST>
-static int launch_bp_tma_t(const BpParams &p, const CUtensorMap &map, bool weighted, int bw, int bh,
-                           int stage_floats, cudaStream_t st) {
-  const size_t smem = sizeof(float) * (size_t)stage_floats * NST + 128;
-  auto kern = weighted ? cone_bp_tma_kernel<true, ZB, NST> : cone_bp_tma_kernel<false, ZB, NST>;
+// Tile pitches: the TMA box width, == 12 or 20 (mod 32) so that an 8 x 4 warp's taps on
+// neighbouring tile rows fall in disjoint banks (scripts/bp_bank_model.py).
+template <int BW>
+static int launch_bp_tma_t(const BpParams &p, const CUtensorMap &map, bool weighted, int bh, int stage_floats, int nst,
+                           cudaStream_t st) {
+  const size_t smem = sizeof(float) * (size_t)stage_floats * nst + 128;
+  auto kern = cone_bp_tma_kernel<BW>;
   TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + ZB - 1) / ZB);
-  kern<<<grid, kBtThreads, smem, st>>>(map, p, bw, bh, stage_floats);
+  dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + 31) / 32);
+  kern<<<grid, kBtThreads, smem, st>>>(map, p, weighted ? 1 : 0, bh, stage_floats, nst,
+                                       kFloorBits * (4u * BW) + 4u * kFloorBits);
   TK_LAUNCHED("cone_bp_tma_kernel");
   return TK_OK;
 }
+
+static const int kBtPitches[] = {44, 52, 76, 84, 108, 116, 140, 148, 172, 180, 204, 212, 236, 244};
 
 int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighted, cudaStream_t st) {
   auto enc = encode_fn();
   if (!enc) return -1;
   if (p.cols % 4 != 0 || (reinterpret_cast<uintptr_t>(p.sino) & 15) != 0) return -1;
   if (p.view_stride != (long long)p.band_rows * p.cols) return -1;
-  const char *ze = getenv("TK_BP_ZB");  // z-voxels per thread: 32 (default) or 16
-  const int zb = ze && atoi(ze) == 16 ? 16 : 32;
-  int bw = 0, bh = 0;
-  footprint_box(p, host_views, zb, bw, bh);
-  if (bw > 256 || bh > 256) return -1;
+  int need = 0, bh = 0;
+  footprint_box(p, host_views, 32, need, bh);
+  int bw = 0;
+  for (int w : kBtPitches)
+    if (w >= need) {
+      bw = w;
+      break;
+    }
+  if (bw == 0 || bh > 256) return -1;
   const int stage_floats = ((bw * bh + 31) / 32) * 32;  // 128-byte aligned stages
   // stages: as many as fit (<= 8) with two CTAs per SM
   int nst = kBtMaxStages;
   while (nst > 2 && sizeof(float) * (size_t)stage_floats * nst + 128 > 110 * 1024) --nst;
   if (sizeof(float) * (size_t)stage_floats * nst + 128 > 110 * 1024) return -1;
-  nst = nst >= 8 ? 8 : nst >= 6 ? 6 : 4;
-  if (nst == 4 && sizeof(float) * (size_t)stage_floats * 4 + 128 > 110 * 1024) return -1;
 
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)p.cols, (cuuint64_t)p.band_rows, (cuuint64_t)p.n_views};
@@ -337,14 +366,22 @@ int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighte
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -1;
-  if (zb == 16) {
-    if (nst == 8) return launch_bp_tma_t<16, 8>(p, map, weighted, bw, bh, stage_floats, st);
-    if (nst == 6) return launch_bp_tma_t<16, 6>(p, map, weighted, bw, bh, stage_floats, st);
-    return launch_bp_tma_t<16, 4>(p, map, weighted, bw, bh, stage_floats, st);
+  switch (bw) {
+    case 44: return launch_bp_tma_t<44>(p, map, weighted, bh, stage_floats, nst, st);
+    case 52: return launch_bp_tma_t<52>(p, map, weighted, bh, stage_floats, nst, st);
+    case 76: return launch_bp_tma_t<76>(p, map, weighted, bh, stage_floats, nst, st);
+    case 84: return launch_bp_tma_t<84>(p, map, weighted, bh, stage_floats, nst, st);
+    case 108: return launch_bp_tma_t<108>(p, map, weighted, bh, stage_floats, nst, st);
+    case 116: return launch_bp_tma_t<116>(p, map, weighted, bh, stage_floats, nst, st);
+    case 140: return launch_bp_tma_t<140>(p, map, weighted, bh, stage_floats, nst, st);
+    case 148: return launch_bp_tma_t<148>(p, map, weighted, bh, stage_floats, nst, st);
+    case 172: return launch_bp_tma_t<172>(p, map, weighted, bh, stage_floats, nst, st);
+    case 180: return launch_bp_tma_t<180>(p, map, weighted, bh, stage_floats, nst, st);
+    case 204: return launch_bp_tma_t<204>(p, map, weighted, bh, stage_floats, nst, st);
+    case 212: return launch_bp_tma_t<212>(p, map, weighted, bh, stage_floats, nst, st);
+    case 236: return launch_bp_tma_t<236>(p, map, weighted, bh, stage_floats, nst, st);
+    default: return launch_bp_tma_t<244>(p, map, weighted, bh, stage_floats, nst, st);
   }
-  if (nst == 8) return launch_bp_tma_t<32, 8>(p, map, weighted, bw, bh, stage_floats, st);
-  if (nst == 6) return launch_bp_tma_t<32, 6>(p, map, weighted, bw, bh, stage_floats, st);
-  return launch_bp_tma_t<32, 4>(p, map, weighted, bw, bh, stage_floats, st);
 }
 
 }  // namespace tk

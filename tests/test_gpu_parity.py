@@ -766,19 +766,19 @@ def test_fp_tuning_knobs_keep_results(tk, monkeypatch, knobs):
     assert rel(got, want.cpu().numpy()) < 1e-6
 
 
-@pytest.mark.parametrize("zb", ["16", "32"])
-def test_bp_tma_z_block_knob(tk, monkeypatch, zb):
-    """TMA back projector with 16 or 32 z-voxels per thread: same result as the quad
-    back projector on a ragged volume (no voxel missed)."""
-    geom = tk.circular_cone_geometry((37, 45, 41), (1.0, 0.9, 1.1), (40, 52), (1.6, 1.5), 33, 2 * np.pi,
-                                     1200.0, 750.0)
-    y = torch.rand(33, 40, 52, device="cuda")
+@pytest.mark.parametrize("det_pitch", [2.4, 1.5, 0.9, 0.5, 0.3])
+def test_bp_tma_tile_pitches(tk, monkeypatch, det_pitch):
+    """TMA back projector across detector pitches that select different compile-time tile
+    pitches (44 ... 244 floats): same result as the quad back projector on a ragged
+    volume, no voxel missed."""
+    geom = tk.circular_cone_geometry((37, 45, 41), (1.0, 0.9, 1.1), (90, 132), (det_pitch, det_pitch), 33,
+                                     2 * np.pi, 1200.0, 750.0)
+    y = torch.rand(33, 90, 132, device="cuda")
     monkeypatch.setenv("TK_BP_ALGO", "quad")
-    want = tk.back_project(tk.Sinogram(y, (1.6, 1.5)), geom, True).data.clone()
+    want = tk.back_project(tk.Sinogram(y, (det_pitch, det_pitch)), geom, True).data.clone()
     monkeypatch.setenv("TK_BP_ALGO", "tma")
-    monkeypatch.setenv("TK_BP_ZB", zb)
     _poison((37, 45, 41))
-    got = tk.back_project(tk.Sinogram(y, (1.6, 1.5)), geom, True).data
+    got = tk.back_project(tk.Sinogram(y, (det_pitch, det_pitch)), geom, True).data
     assert bool(torch.isfinite(got).all())
     assert rel(got, want.cpu().numpy()) < 1e-5
 
