@@ -15,4 +15,6 @@ mkdir -p "$ROOT/baseline/_ref/ref_tests"
 cp -r "$REF/pkg/tests" "$ROOT/baseline/_ref/ref_tests/pkg_tests"
 cp -r "$REF/pkg/bindings/tests" "$ROOT/baseline/_ref/ref_tests/bindings_tests"
 cp -r "$REF/pkg/configs" "$ROOT/baseline/_ref/ref_tests/configs" 2>/dev/null || true
+# test_acceptance.py criterion 7 runs pkg/scripts/artifact_gallery.py relative to its own directory
+cp -r "$REF/pkg/scripts" "$ROOT/baseline/_ref/ref_tests/scripts" 2>/dev/null || true
 echo "installed tomokit into $ROOT/baseline/_ref"

@@ -75,6 +75,10 @@ def main():
     import pytest
 
     tests = REF / "ref_tests"
+    # importlib mode does not put test directories on sys.path; the suites import siblings
+    # (test_acceptance.py: `from test_geometry import ...`)
+    sys.path.insert(0, str(tests / "pkg_tests"))
+    sys.path.insert(0, str(tests / "bindings_tests"))
     files = [tests / "pkg_tests" / f for f in ("test_projectors.py", "test_filters.py", "test_autodiff.py",
                                                 "test_acceptance.py", "test_geometry.py", "test_grids.py",
                                                 "test_phantoms.py", "test_artifacts.py")]
