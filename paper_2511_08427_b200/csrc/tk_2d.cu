@@ -158,7 +158,7 @@ struct Bp2View {  // per-angle float32 constants
 template <bool FAN, bool WEIGHTED>
 __global__ void __launch_bounds__(256)
     bp2d_kernel(const float *__restrict__ sino, int n_ang, int n_det,
-                const Bp2View *__restrict__ views, float half, float sdd_over_ds, float sid,
+                const Bp2View *__restrict__ views, float hfrac, int hint, float sdd_over_ds, float sid,
                 int nx, int ny, float sx, float sy, float *__restrict__ out) {
   __shared__ Bp2View sv[256];
   const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -176,22 +176,22 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < nch; ++j) {
       const Bp2View V = sv[j];
       const float *row = sino + (long long)(a0 + j) * n_det;
-      float f, q = 1.f;
+      float t, q = 1.f;  // detector coordinate relative to the centre (fp32 stays fine for wide detectors)
       if (!FAN) {
-        f = fmaf(x, V.c, fmaf(y, V.s, half));
+        t = fmaf(x, V.c, y * V.s);
       } else {
         const float w = sid - x * V.c - y * V.s;
         if (!(w > 1e-12f)) continue;
         const float rw = 1.f / w;
-        f = fmaf(sdd_over_ds * (y * V.c - x * V.s), rw, half);
+        t = sdd_over_ds * (y * V.c - x * V.s) * rw;
         if (WEIGHTED) {
           q = sid * rw;
           q *= q;
         }
       }
-      const float fl = floorf(f);
-      const int j0 = (int)fl;
-      const float w = f - fl;
+      const float tt = t + hfrac, fl = floorf(tt);  // f = tt + hint, hint integer
+      const int j0 = (int)fl + hint;
+      const float w = tt - fl;
       const float g0 = ((unsigned)j0 < (unsigned)n_det) ? 1.f - w : 0.f;
       const float g1 = ((unsigned)(j0 + 1) < (unsigned)n_det) ? w : 0.f;
       const int ja = min(max(j0, 0), n_det - 1), jb = min(max(j0 + 1, 0), n_det - 1);
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(256)
 constexpr int kBt2Max = 12288;
 template <bool FAN, bool WEIGHTED, bool SMEM>
 __global__ void __launch_bounds__(256)
-    bp2d_adjoint_kernel(const float *__restrict__ img, int n_det, const Bp2View *__restrict__ views, float half,
-                        float sdd_over_ds, float sid, int nx, int ny, float sx, float sy,
+    bp2d_adjoint_kernel(const float *__restrict__ img, int n_det, const Bp2View *__restrict__ views, float hfrac,
+                        int hint, float sdd_over_ds, float sid, int nx, int ny, float sx, float sy,
                         float *__restrict__ sino) {
   extern __shared__ float row_acc[];
   const int a = blockIdx.x;
@@ -228,22 +228,22 @@ __global__ void __launch_bounds__(256)
     const int ix = (int)(i % nx), iy = (int)(i / nx);
     const float x = ((float)ix - (nx - 1) * 0.5f) * sx;
     const float y = ((float)iy - (ny - 1) * 0.5f) * sy;
-    float f, q = 1.f;
+    float t, q = 1.f;
     if (!FAN) {
-      f = fmaf(x, V.c, fmaf(y, V.s, half));
+      t = fmaf(x, V.c, y * V.s);
     } else {
       const float w = sid - x * V.c - y * V.s;
       if (!(w > 1e-12f)) continue;
       const float rw = 1.f / w;
-      f = fmaf(sdd_over_ds * (y * V.c - x * V.s), rw, half);
+      t = sdd_over_ds * (y * V.c - x * V.s) * rw;
       if (WEIGHTED) {
         q = sid * rw;
         q *= q;
       }
     }
-    const float fl = floorf(f);
-    const int j0 = (int)fl;
-    const float w = f - fl, gq = g * q;
+    const float tt = t + hfrac, fl = floorf(tt);
+    const int j0 = (int)fl + hint;
+    const float w = tt - fl, gq = g * q;
     if ((unsigned)j0 < (unsigned)n_det) atomicAdd(row + j0, (1.f - w) * gq);
     if ((unsigned)(j0 + 1) < (unsigned)n_det) atomicAdd(row + j0 + 1, w * gq);
   }
@@ -310,14 +310,18 @@ static int bp2d(bool fan, const float *sino, int n_ang, int n_det, const double 
   Scratch d;
   TK_TRY_CUDA(upload(d, h.data(), sizeof(Bp2View) * n_ang, st));
   dim3 grid(ceil_div(nx, 32), ceil_div(ny, 8));
-  const float half = (float)((n_det - 1) / 2.0);
+  const int hint = (n_det - 1) / 2;  // detector centre (n_det - 1) / 2 = hint + hfrac, hfrac in {0, 1/2}
+  const float hfrac = (n_det - 1) % 2 ? 0.5f : 0.f;
   const float sdd_ds = (float)(sdd / ds);
   if (!fan)
-    bp2d_kernel<false, false><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), half, 0.f, 0.f, nx, ny, (float)sx, (float)sy, out);
+    bp2d_kernel<false, false><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), hfrac, hint, 0.f, 0.f, nx, ny,
+                                                    (float)sx, (float)sy, out);
   else if (weighted)
-    bp2d_kernel<true, true><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), half, sdd_ds, (float)sid, nx, ny, (float)sx, (float)sy, out);
+    bp2d_kernel<true, true><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), hfrac, hint, sdd_ds, (float)sid,
+                                                  nx, ny, (float)sx, (float)sy, out);
   else
-    bp2d_kernel<true, false><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), half, sdd_ds, (float)sid, nx, ny, (float)sx, (float)sy, out);
+    bp2d_kernel<true, false><<<grid, 256, 0, st>>>(sino, n_ang, n_det, d.as<Bp2View>(), hfrac, hint, sdd_ds, (float)sid,
+                                                   nx, ny, (float)sx, (float)sy, out);
   TK_LAUNCHED("bp2d_kernel");
   return TK_OK;
 }
@@ -339,7 +343,8 @@ static int bp2d_adjoint(bool fan, const float *img, int ny, int nx, double sy, d
   }
   Scratch d;
   TK_TRY_CUDA(upload(d, h.data(), sizeof(Bp2View) * n_ang, st));
-  const float half = (float)((n_det - 1) / 2.0), sdd_ds = (float)(sdd / ds);
+  const int hint = (n_det - 1) / 2;  // detector centre (n_det - 1) / 2 = hint + hfrac, hfrac in {0, 1/2}
+  const float hfrac = (n_det - 1) % 2 ? 0.5f : 0.f, sdd_ds = (float)(sdd / ds);
   const bool smem = n_det <= kBt2Max;
   const size_t sb = smem ? sizeof(float) * n_det : 0;
   if (!smem) TK_TRY_CUDA(cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)n_ang * n_det, st));
@@ -347,7 +352,7 @@ static int bp2d_adjoint(bool fan, const float *img, int ny, int nx, double sy, d
                               : (smem ? bp2d_adjoint_kernel<true, false, true> : bp2d_adjoint_kernel<true, false, false>))
                   : (smem ? bp2d_adjoint_kernel<false, false, true> : bp2d_adjoint_kernel<false, false, false>);
   if (sb > 48 * 1024) TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-  kern<<<n_ang, 256, sb, st>>>(img, n_det, d.as<Bp2View>(), half, sdd_ds, (float)sid, nx, ny, (float)sx, (float)sy,
+  kern<<<n_ang, 256, sb, st>>>(img, n_det, d.as<Bp2View>(), hfrac, hint, sdd_ds, (float)sid, nx, ny, (float)sx, (float)sy,
                                sino);
   TK_LAUNCHED("bp2d_adjoint_kernel");
   return TK_OK;

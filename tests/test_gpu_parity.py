@@ -471,11 +471,16 @@ def test_2d_bp_transpose_matches_oracle(tk, oracle):
         assert rel(got, oracle.back_fan_2d_T(x, angf, 1200.0, 750.0, 1.6, 70, (0.9, 1.1), w)) < TOL
     for g in (gp, gf):
         assert tk.dot_test(tk.back_projection_op(g, matched=True), trials=3) <= 1e-4
-    # wide detector: global-atomic path (rows longer than the shared-memory row buffer)
+    # wide detector: global-atomic path (rows longer than the shared-memory row buffer);
+    # detector coordinates are formed relative to the centre, so fp32 keeps the
+    # interpolation weights accurate 6500 pixels out
     gw = tk.GeometryParallel2D((24, 24), (1.0, 1.0), 13000, 0.01, ang[:5])
     xw = rng.standard_normal((24, 24))
     got = tk.transpose_back_project(tk.Volume(xw, (1.0, 1.0)), gw).data
     assert rel(got, oracle.back_parallel_2d_T(xw, ang[:5], 0.01, 13000, (1.0, 1.0))) < TOL
+    yw = rng.standard_normal((5, 13000))
+    got = tk.back_project(tk.Sinogram(yw, (0.01,)), gw).data
+    assert rel(got, oracle.back_parallel_2d(yw, ang[:5], 0.01, (24, 24), (1.0, 1.0))) < TOL
     y = torch.tensor(rng.standard_normal((61, 70)), dtype=torch.float32, device="cuda", requires_grad=True)
     out = tk.FanBackProjection2D.apply(y, gf, "matched", True)
     gx = torch.randn_like(out)
