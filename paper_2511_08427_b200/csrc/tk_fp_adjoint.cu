@@ -11,6 +11,12 @@
 // deterministic.  Deterministic mode: 64-bit fixed-point quads with integer
 // atomics (associative: bit-reproducible), scale chosen from max |y| and a
 // geometric bound on the contributions per tap so no sum can overflow.
+//
+// Bound: the L2 vector-reduction pipeline (cfg5: 2.0e11 reduction sectors, atomic input
+// 59 % busy, half the sectors miss L2).  Measured at cfg5 (profiles/r02): pair arithmetic
+// (FFMA2 weights, 4 FFMA2 accumulations per sample) 1002 -> 984 ms; without the row
+// carry-over 1300 ms; rays split into 2 / 3 / 4 / 6 launches by segment (smaller working set
+// of the reduction targets) 1014 / 1036 / 1053 / 1082 ms -- not kept.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -45,7 +51,7 @@ __device__ __forceinline__ void red_add_fx4(unsigned long long *p, const float4 
   atomicAdd(p + 3, (unsigned long long)__float2ll_rn(v.w * scale));
 }
 
-template <int MINB, bool DET = false>
+template <int MINB, bool DET = false, bool CARRY = true>
 __global__ void __launch_bounds__(128, MINB)
     cone_fp_adjoint4z_kernel(const float *__restrict__ sino, void *__restrict__ qy_, void *__restrict__ qx_,
                              int nx, int ny, int nz, double sx, double sy, double sz,
@@ -68,12 +74,6 @@ __global__ void __launch_bounds__(128, MINB)
   if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
   const bool xrow = fabsf(rs.gx) > fabsf(rs.gy);  // major horizontal axis (cells per step)
   void *qv = xrow ? qx_ : qy_;
-  auto flush = [&](unsigned cidx, const float4 &v) {  // quad cidx += v
-    if (DET)
-      red_add_fx4(static_cast<unsigned long long *>(qv) + 4ull * cidx, v, scale);
-    else
-      red_add_v4(static_cast<float4 *>(qv) + cidx, v);
-  };
   const float ea = (xrow ? rs.ey : rs.ex) + (kFpMargin - 1), eb = (xrow ? rs.ex : rs.ey) + (kFpMargin - 1);
   const float ez = rs.ez + (kFpMargin - 1);
   const float ga = xrow ? rs.gy : rs.gx, gb = xrow ? rs.gx : rs.gy, gz = rs.gz;
@@ -81,54 +81,68 @@ __global__ void __launch_bounds__(128, MINB)
   const unsigned sas = pz, sbs = (unsigned)((xrow ? ny : nx) + 2 * kFpMargin) * pz;  // a and b strides
   const unsigned bias = kFloorBits * (1u + sas + sbs);
   const float g = y * (float)step;
-  float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-  unsigned cell = 0u;
-  bool open = false;
+  // (a, b) position / floor / fraction as FFMA2 / FADD2 pairs; weights as pairs (1 - w, w);
+  // the 8 accumulators as 4 pairs, each sample 4 FFMA2 (broadcast row-weight x (1 - wa, wa))
+  const unsigned long long e2 = pk2(ea, eb), g2 = pk2(ga, gb), m2 = pk2(kFloorMagic, kFloorMagic);
+  const unsigned long long one0 = pk2(1.f, 0.f), m1p1 = pk2(-1.f, 1.f);
+  unsigned long long lo01 = 0ull, lo23 = 0ull, hi01 = 0ull, hi23 = 0ull;  // quads (row b, row b + 1)
+  auto cell_of = [&](float kk) -> unsigned {
+    const unsigned long long fab = ffma2(pk2(kk, kk), g2, e2);
+    const float2 xab = upk2(fadd2_rm(fab, m2));
+    const float xz = floor_magic(fmaf(kk, gz, ez));
+    return __float_as_uint(xab.y) * sbs + (__float_as_uint(xab.x) * sas + __float_as_uint(xz));
+  };
+  auto flush = [&](unsigned cidx, unsigned long long q01, unsigned long long q23) {  // quad cidx += q
+    const float2 a = upk2(q01), c = upk2(q23);
+    const float4 v = make_float4(a.x, a.y, c.x, c.y);
+    if (DET)
+      red_add_fx4(static_cast<unsigned long long *>(qv) + 4ull * cidx, v, scale);
+    else
+      red_add_v4(static_cast<float4 *>(qv) + cidx, v);
+  };
+  unsigned cell = cell_of(0.5f);  // the first sample's cell: no flush before it
   auto sample = [&](float kk, float gs) {
-    const float fa = fmaf(kk, ga, ea), fb = fmaf(kk, gb, eb), fz = fmaf(kk, gz, ez);
-    const float xa = floor_magic(fa), xb = floor_magic(fb), xz = floor_magic(fz);
-    const unsigned id = __float_as_uint(xb) * sbs + (__float_as_uint(xa) * sas + __float_as_uint(xz));
+    const unsigned long long fab = ffma2(pk2(kk, kk), g2, e2);
+    const float fz = fmaf(kk, gz, ez);
+    const unsigned long long xab = fadd2_rm(fab, m2);
+    const float xz = floor_magic(fz);
+    const float2 xb = upk2(xab);
+    const unsigned id = __float_as_uint(xb.y) * sbs + (__float_as_uint(xb.x) * sas + __float_as_uint(xz));
     if (id != cell) {
-      const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (open) {
-        const unsigned c0 = cell - bias;
-        const unsigned d = id - cell;
-        if (d == sbs) {  // row b -> b + 1: the far row becomes the near row
-          flush(c0, lo);
-          lo = hi;
-          hi = zero;
-        } else if (d == 0u - sbs) {  // row b -> b - 1: the near row becomes the far row
-          flush(c0 + sbs, hi);
-          hi = lo;
-          lo = zero;
-        } else {
-          flush(c0, lo);
-          flush(c0 + sbs, hi);
-          lo = hi = zero;
-        }
+      const unsigned c0 = cell - bias;
+      if (CARRY && id == cell + sbs) {  // row b -> b + 1: the far row becomes the near row
+        flush(c0, lo01, lo23);
+        lo01 = hi01, lo23 = hi23, hi01 = 0ull, hi23 = 0ull;
+      } else if (CARRY && id + sbs == cell) {  // row b -> b - 1: the near row becomes the far row
+        flush(c0 + sbs, hi01, hi23);
+        hi01 = lo01, hi23 = lo23, lo01 = 0ull, lo23 = 0ull;
+      } else {
+        flush(c0, lo01, lo23);
+        flush(c0 + sbs, hi01, hi23);
+        lo01 = lo23 = hi01 = hi23 = 0ull;
       }
-      open = true;
       cell = id;
     }
-    const float wa = fa - (xa - kFloorMagic), wb = fb - (xb - kFloorMagic), wz = fz - (xz - kFloorMagic);
-    const float g1 = gs * wb, g0 = gs - g1;
-    const float l1 = g0 * wz, l0 = g0 - l1, h1 = g1 * wz, h0 = g1 - h1;
-    const float l0a = l0 * wa, l1a = l1 * wa, h0a = h0 * wa, h1a = h1 * wa;
-    lo.x += l0 - l0a;
-    lo.y += l0a;
-    lo.z += l1 - l1a;
-    lo.w += l1a;
-    hi.x += h0 - h0a;
-    hi.y += h0a;
-    hi.z += h1 - h1a;
-    hi.w += h1a;
+    const float2 w = upk2(fsub2(fab, fsub2(xab, m2)));  // (wa, wb)
+    const float wz = fz - (xz - kFloorMagic);
+    const unsigned long long pa = ffma2(pk2(w.x, w.x), m1p1, one0);  // (1 - wa, wa)
+    const unsigned long long pb = ffma2(pk2(w.y, w.y), m1p1, one0);  // (1 - wb, wb)
+    const unsigned long long pzw = ffma2(pk2(wz, wz), m1p1, one0);   // (1 - wz, wz)
+    const float2 gg = upk2(fmul2(pk2(gs, gs), pb));                 // (g0, g1): rows b, b + 1
+    const float2 l = upk2(fmul2(pk2(gg.x, gg.x), pzw));             // (l0, l1): slices z, z + 1 of row b
+    const float2 h = upk2(fmul2(pk2(gg.y, gg.y), pzw));             // (h0, h1): of row b + 1
+    lo01 = ffma2(pk2(l.x, l.x), pa, lo01);
+    lo23 = ffma2(pk2(l.y, l.y), pa, lo23);
+    hi01 = ffma2(pk2(h.x, h.x), pa, hi01);
+    hi23 = ffma2(pk2(h.y, h.y), pa, hi23);
   };
-  float kf = 0.5f;
   const int nfull = rs.n - 1;
+  float kf = 0.5f;
+#pragma unroll 2
   for (int k = 0; k < nfull; ++k, kf += 1.f) sample(kf, g);
   sample((float)nfull + 0.5f * rs.last, g * rs.last);
-  flush(cell - bias, lo);
-  flush(cell - bias + sbs, hi);
+  flush(cell - bias, lo01, lo23);
+  flush(cell - bias + sbs, hi01, hi23);
 }
 
 // deterministic fold: vol[z][y][x] = 2^-e (sum of the 8 fixed-point taps of both
@@ -343,8 +357,11 @@ static int launch_fp_adjoint(const float *sino, int nz, int ny, int nx, double s
   TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, sizeof(float4) * ncell, st));
   const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
   if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
-  cone_fp_adjoint4z_kernel<8><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
-                                                             dviews.as<ConeRayView>(), rows, cols, n_views, step, 1.f);
+  // TK_FPT_CARRY (default 1): carry the far-row quad over on row steps (one reduction instead of two)
+  const char *ce = getenv("TK_FPT_CARRY");
+  auto kern = (ce && !atoi(ce)) ? cone_fp_adjoint4z_kernel<8, false, false> : cone_fp_adjoint4z_kernel<8>;
+  kern<<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz, dviews.as<ConeRayView>(), rows,
+                                      cols, n_views, step, 1.f);
   TK_LAUNCHED("cone_fp_adjoint4z_kernel");
   unquad_z_kernel<<<dim3(ceil_div(nz, 32), ceil_div(nx, 32), ny), 256, 0, st>>>(qA.as<float4>(), nz, ny, nx, vol);
   TK_LAUNCHED("unquad_z_kernel");

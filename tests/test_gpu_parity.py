@@ -443,7 +443,10 @@ def test_fp_variants_match_oracle(tk, oracle, monkeypatch, knobs):
     assert rel(got, g.forward_cone_3d(x, (0.9, 1.1, 1.0), gl.matrix_array(), (30, 34), 0.45)) < TOL
 
 
-def test_fp_transpose_matches_oracle(tk, oracle):
+@pytest.mark.parametrize("knobs", [{}, {"TK_FPT_CARRY": "0"}])
+def test_fp_transpose_matches_oracle(tk, oracle, monkeypatch, knobs):
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
     shape, sp = (20, 26, 22), (1.1, 0.9, 1.0)
     hel = tk.helical_trajectory_3d(11, 4 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4), -8.0, 8.0)
     for mats in (hel, tk.circular_trajectory_3d(13, 2 * np.pi, 1200.0, 750.0, (30, 34), (1.5, 1.4))):
