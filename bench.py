@@ -63,9 +63,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--fdk", choices=["zslab", "angle"], default="zslab",
-                    help="N>1 FDK decomposition: z-slabs fed by a row-band all-to-all, or angle shards "
-                         "+ reduce-scatter")
+    ap.add_argument("--fdk", choices=["zslab", "p2p", "angle"], default="zslab",
+                    help="N>1 FDK decomposition: z-slabs fed by a row-band all-to-all (zslab) or by the "
+                         "forward-projection kernel storing rays into peers' band buffers (p2p, NVLink "
+                         "symmetric memory), or angle shards + reduce-scatter")
     ap.add_argument("--chunks", type=int, default=4, help="N>1: view chunks of the FP/all-to-all pipeline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,6 +83,9 @@ def config(world: int, fdk: str, chunks: int) -> dict:
     elif fdk == "zslab":
         par = (f"dp{world}: FP views/{world}; FDK z-slabs/{world} fed by an uneven NCCL all-to-all of "
                f"detector row bands in {chunks} view chunks")
+    elif fdk == "p2p":
+        par = (f"dp{world}: FP views/{world} storing each ray into the owning ranks' row-band buffers over "
+               f"NVLink peer memory (symmetric memory, no collective); FDK z-slabs/{world}")
     else:
         par = f"dp{world}: FP views/{world}; FDK angle shards/{world} + NCCL reduce-scatter of the volume"
     return {"workload": WORKLOAD, "volume": list(VOL), "views": VIEWS, "detector": list(DET),
@@ -472,6 +476,7 @@ def run_ours(args):
     bands = D.slab_bands(geom, world)
     z0, z1, r0, r1 = bands[rank]
     angle = world > 1 and args.fdk == "angle"
+    p2p = world > 1 and args.fdk == "p2p"
     if angle:
         z0, z1 = rank * VOL[0] // world, (rank + 1) * VOL[0] // world
     n_chunks = max(1, args.chunks) if world > 1 else 1
@@ -510,6 +515,14 @@ def run_ours(args):
             filter_stage_tensor(sino, geom, FILTER, out=filt)
             rec(3)
             _, slab = D.fdk_angle_sharded(filt, geom, FILTER, rank, world, filter_fn=lambda s: s)
+        elif p2p:
+            got = D.forward_project_p2p(vol, geom, step, rank, world, bands=bands)
+            rec(1)
+            rec(2)
+            filter_stage_tensor(got, geom, FILTER, out=band, row_offset=r0)
+            rec(3)
+            bp_cone_tensor_ex(band, geom, True, r0, z0, z1 - z0, out=slab)
+            slab.mul_(math.pi / VIEWS)
         else:
             _, order = D.forward_project_and_exchange(
                 vol, geom, step, rank, world, n_chunks=n_chunks, bands=bands, out=band_raw,
@@ -572,8 +585,9 @@ def run_ours(args):
                                    "gups": round(NVOX * (ve - vb) / (fp_ms * 1e-3) / 1e9, 2),
                                    "samples": samples, "gsamples_per_s": round(samples / (fp_ms * 1e-3) / 1e9, 2)},
             "exchange": {"ms": round(xchg_ms, 3),
-                         "what": "none" if world == 1 else ("row-band all-to-all tail after the last FP chunk"
-                                                            if not angle else "none (angle shards)"),
+                         "what": "none" if world == 1 else ("none (angle shards)" if angle else
+                                                            "peer stores inside the FP kernel + barrier" if p2p
+                                                            else "row-band all-to-all tail after the last FP chunk"),
                          "recv_bytes_per_rank": 0 if world == 1 or angle else
                          4 * DET[1] * VIEWS * (r1 - r0) * (world - 1) // world},
             "filter": {"ms": round(filt_ms, 3)},

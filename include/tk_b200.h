@@ -92,6 +92,17 @@ int tk_forward_cone_3d(const float *vol, int nz, int ny, int nx, double sz,
  * no device work): 1 = the z-mirror-pair kernel (every view z-mirror
  * symmetric -- circular orbits with the principal row at (R-1)/2 -- and the
  * volume fits its layout), 0 = the general ray-per-thread kernel. */
+/* View-sharded forward projection fused with the multi-GPU row-band exchange
+ * (no reference counterpart; distributed.py): ray (v, r, c) of these n_views views is
+ * stored into every destination h whose detector row band [r0[h], r1[h]) holds row r, at
+ * dest[h] + ((view_offset + v) * band_pitch_rows + (r - r0[h])) * cols + c.  dest[h] may be
+ * a peer GPU's buffer (CUDA IPC / symmetric memory over NVLink): the stores are the
+ * exchange, issued ray by ray as the projection runs.  1..16 destinations. */
+int tk_forward_cone_3d_bands(const float *vol, int nz, int ny, int nx, double sz, double sy,
+                             double sx, const double *sources, const double *minv, int n_views,
+                             int rows, int cols, double step, int view_offset, int n_dest,
+                             float *const *dest, const int *r0, const int *r1,
+                             int band_pitch_rows, void *stream);
 int tk_forward_cone_3d_path(const double *sources, const double *minv, int n_views, int rows,
                             int cols, int nz, int ny, int nx);
 /* Forward-projection plan (no reference counterpart): the per-volume

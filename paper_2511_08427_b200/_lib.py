@@ -42,6 +42,9 @@ SIGNATURES = {
                        _c_dbl, _c_dbl, _c_int, _ptr, _ptr],
     "tk_forward_cone_3d": [_ptr, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl, _dptr, _dptr,
                            _c_int, _c_int, _c_int, _c_dbl, _ptr, _ptr],
+    "tk_forward_cone_3d_bands": [_ptr, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl, _dptr, _dptr, _c_int,
+                                 _c_int, _c_int, _c_dbl, _c_int, _c_int, ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), _c_int, _ptr],
     "tk_forward_cone_3d_path": [_dptr, _dptr, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int],
     "tk_fp_plan_create": [_ptr, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl,
                           ctypes.POINTER(ctypes.c_void_p), _ptr],

@@ -153,11 +153,24 @@ __device__ __forceinline__ void ldg_pair4(const Pair4 *p, unsigned ys, Pair4 &lo
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-template <int VG, int CPS, bool FIXS>
-__global__ void __launch_bounds__(128 * VG, CPS)
-    cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
-                   const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
-                   float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+// Row-band destinations of the fused multi-GPU forward projection (BANDS = true):
+// ray (v, r, c) is stored into every rank h whose band [r0[h], r1[h]) holds row r,
+// at ptr[h][(view_offset + v) * view_stride + (r - r0[h]) * cols + c].  ptr[h] is a
+// peer (NVLink P2P) or local address: the stores ARE the exchange, issued ray by ray
+// as the projection proceeds.
+constexpr int kFpMaxDest = 16;
+struct FpDests {
+  float *ptr[kFpMaxDest];
+  int r0[kFpMaxDest], r1[kFpMaxDest];
+  int n, view_offset;
+  long long view_stride;
+};
+
+template <int VG, bool FIXS, bool BANDS>
+__device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
+                                        double sz, const ConeRayView *__restrict__ views, int rows, int cols,
+                                        int n_views, double step, float *__restrict__ out, unsigned zpitch,
+                                        unsigned ystride, const FpDests *dests) {
   const int ncb = (cols + kFpCols - 1) / kFpCols;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
@@ -167,10 +180,21 @@ __global__ void __launch_bounds__(128 * VG, CPS)
   const int sub = threadIdx.x >> 7, t = threadIdx.x & 127;
   const int v = v0 + sub, c = cb * kFpCols + (t >> 3), r = rb * kFpRows + (t & 7);
   if (c >= cols || r >= rows || v >= n_views) return;
-  float *dst = out + ((long long)v * rows + r) * cols + c;
+  float *dst = BANDS ? nullptr : out + ((long long)v * rows + r) * cols + c;
+  auto store = [&](float val) {
+    if (BANDS) {
+#pragma unroll 1
+      for (int h = 0; h < dests->n; ++h)
+        if (r >= dests->r0[h] && r < dests->r1[h])
+          dests->ptr[h][(long long)(dests->view_offset + v) * dests->view_stride +
+                        (long long)(r - dests->r0[h]) * cols + c] = val;
+    } else {
+      *dst = val;
+    }
+  };
   RaySetup rs;
   if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
-    *dst = 0.f;
+    store(0.f);
     return;
   }
   const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
@@ -206,7 +230,25 @@ __global__ void __launch_bounds__(128 * VG, CPS)
 #pragma unroll 2
   for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
   acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
-  *dst = acc * (float)step;
+  store(acc * (float)step);
+}
+
+template <int VG, int CPS, bool FIXS>
+__global__ void __launch_bounds__(128 * VG, CPS)
+    cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
+                   const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
+                   float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+  fp_rays<VG, FIXS, false>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride, nullptr);
+}
+
+// The same march storing into row-band destinations (tk_forward_cone_3d_bands).
+template <bool FIXS>
+__global__ void __launch_bounds__(1024, 2)
+    cone_fp_bands_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
+                         const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
+                         unsigned zpitch, unsigned ystride, const __grid_constant__ FpDests dests) {
+  fp_rays<8, FIXS, true>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, nullptr, zpitch, ystride,
+                         &dests);
 }
 
 // Sub-block = 16 columns x 8 direct rows (lower detector half) plus their 8 mirror rows.
@@ -526,6 +568,28 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
   return TK_OK;
 }
 
+// Fused view-sharded projection + row-band exchange: the general kernel with BANDS stores.
+static int plan_project_bands(FpPlan &pl, const double *sources, const double *minv, int n_views, int rows, int cols,
+                              double step, const FpDests &d, cudaStream_t st) {
+  int rc = plan_cells(pl, false, st);
+  if (rc != TK_OK) return rc;
+  const FpLayout &L = pl.lay[0];
+  std::vector<ConeRayView> hv(n_views);
+  for (int i = 0; i < n_views; ++i) {
+    for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
+    for (int j = 0; j < 9; ++j) hv[i].minv[j] = minv[9 * i + j];
+  }
+  Scratch dviews;
+  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
+  const long long nb = (long long)ceil_div(cols, kFpCols) * ceil_div(rows, kFpRows) * ceil_div(n_views, 8);
+  if (nb >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_bands: problem too large for one launch");
+  auto kern = L.fixs ? cone_fp_bands_kernel<true> : cone_fp_bands_kernel<false>;
+  kern<<<(unsigned)nb, 1024, 0, st>>>(static_cast<const float4 *>(pl.cells[0]), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
+                                      dviews.as<ConeRayView>(), rows, cols, n_views, step, L.zpitch, L.ystride, d);
+  TK_LAUNCHED("cone_fp_bands_kernel");
+  return TK_OK;
+}
+
 static int launch_fp_default(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
                       const double *sources, const double *minv, int n_views, int rows, int cols, double step,
                       float *out, cudaStream_t st) {
@@ -595,6 +659,37 @@ int tk_fp_plan_destroy(void *plan, void *stream) {
   plan_free(*pl, as_stream(stream));
   delete pl;
   return TK_OK;
+}
+
+int tk_forward_cone_3d_bands(const float *vol, int nz, int ny, int nx, double sz, double sy, double sx,
+                             const double *sources, const double *minv, int n_views, int rows, int cols, double step,
+                             int view_offset, int n_dest, float *const *dest, const int *r0, const int *r1,
+                             int band_pitch_rows, void *stream) {
+  clear_error();
+  if (!vol || !sources || !minv || !dest || !r0 || !r1) return fail_arg("tk_forward_cone_3d_bands: null pointer");
+  if (nz < 1 || ny < 1 || nx < 1 || n_views < 1 || rows < 1 || cols < 1 || view_offset < 0)
+    return fail_arg("tk_forward_cone_3d_bands: non-positive extent");
+  if (!(sx > 0 && sy > 0 && sz > 0 && step > 0)) return fail_arg("tk_forward_cone_3d_bands: spacing/step must be > 0");
+  if (n_dest < 1 || n_dest > kFpMaxDest) return fail_arg("tk_forward_cone_3d_bands: 1 to 16 destinations");
+  FpDests d{};
+  d.n = n_dest;
+  d.view_offset = view_offset;
+  d.view_stride = (long long)band_pitch_rows * cols;
+  for (int h = 0; h < n_dest; ++h) {
+    if (!dest[h]) return fail_arg("tk_forward_cone_3d_bands: null destination");
+    if (r0[h] < 0 || r1[h] > rows || r1[h] - r0[h] > band_pitch_rows)
+      return fail_arg("tk_forward_cone_3d_bands: band outside the detector or wider than the pitch");
+    d.ptr[h] = dest[h];
+    d.r0[h] = r0[h];
+    d.r1[h] = r1[h];
+  }
+  FpPlan pl;
+  pl.vol = vol;
+  pl.nz = nz, pl.ny = ny, pl.nx = nx;
+  pl.sz = sz, pl.sy = sy, pl.sx = sx;
+  const int rc = plan_project_bands(pl, sources, minv, n_views, rows, cols, step, d, as_stream(stream));
+  plan_free(pl, as_stream(stream));
+  return rc;
 }
 
 int tk_forward_cone_3d_path(const double *sources, const double *minv, int n_views, int rows, int cols, int nz,

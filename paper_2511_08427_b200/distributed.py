@@ -14,6 +14,10 @@ reference is single-process):
   only the detector row band its slab projects into (band from the slab's
   corner projections through every P), so output slabs are disjoint and need
   no reduction;
+* fused path (`forward_project_p2p`) -- the forward projection kernel itself
+  stores each ray into the band buffers of the ranks whose z-slab needs its row,
+  through peer (NVLink) addresses of symmetric-memory buffers: no separate
+  collective, the exchange overlaps the projection ray by ray;
 * comparison path -- angle-sharded back projection into full partial volumes
   followed by a reduce / reduce-scatter of the volume.
 
@@ -45,6 +49,7 @@ __all__ = [
     "received_view_order",
     "exchange_row_bands",
     "forward_project_and_exchange",
+    "forward_project_p2p",
     "fdk_angle_sharded",
 ]
 
@@ -304,6 +309,54 @@ def forward_project_and_exchange(vol: torch.Tensor, geom: GeometryCone3D, step: 
         if work is not None:
             work.wait()
     return out, received_view_order(nv, world, n_chunks)
+
+
+_symm_cache: dict = {}
+
+
+def _band_buffers(shape, device, group):
+    """A symmetric-memory (peer-addressable) fp32 buffer of ``shape`` on every rank and the
+    list of every rank's buffer address (torch.distributed._symmetric_memory, CUDA IPC over
+    NVLink); cached per (shape, device, group) -- allocation and rendezvous are collective."""
+    import torch.distributed._symmetric_memory as symm
+
+    group = group or dist.group.WORLD
+    key = (tuple(shape), device.index, id(group))
+    hit = _symm_cache.get(key)
+    if hit is None:
+        buf = symm.empty(shape, dtype=torch.float32, device=device)
+        hdl = symm.rendezvous(buf, group)
+        hit = _symm_cache[key] = (buf, hdl, [int(p) for p in hdl.buffer_ptrs])
+    return hit
+
+
+def forward_project_p2p(vol: torch.Tensor, geom: GeometryCone3D, step: float, rank: int, world: int,
+                        bands=None, group=None, fp_bands_fn: Callable | None = None):
+    """View-sharded forward projection fused with the row-band exchange.
+
+    Rank g projects its view block and the kernel stores every ray straight into the
+    band buffer of each rank h whose row band [r0_h, r1_h) holds the ray's detector row
+    -- a peer address on another GPU (symmetric memory over NVLink), so the exchange
+    IS the projection's output stores and needs no collective; a device-side barrier
+    then makes all peers' stores visible.  Views land at their global index (no
+    reordering).  Returns this rank's band (V, r1 - r0, cols), a view of the
+    (V, max band rows, cols) symmetric buffer.
+    """
+    if fp_bands_fn is None:
+        from .projectors import fp_bands_tensor as fp_bands_fn
+    nv = geom.n_projections
+    bands = bands or slab_bands(geom, world)
+    rows, cols = geom.detector_shape
+    pitch = max(r1 - r0 for (_, _, r0, r1) in bands)
+    buf, hdl, ptrs = _band_buffers((nv, pitch, cols), vol.device, group)
+    vb, ve = shard_bounds(nv, world, rank)
+    hdl.barrier()  # every rank is done reading its band from the previous call
+    if ve > vb:
+        fp_bands_fn(vol, subset_geometry(geom, slice(vb, ve)), step, vb, ptrs,
+                    [(r0, r1) for (_, _, r0, r1) in bands], pitch)
+    hdl.barrier()  # all peers' stores into this rank's band are visible
+    _, _, r0, r1 = bands[rank]
+    return buf[:, : r1 - r0]
 
 
 def fdk_angle_sharded(sino_local: torch.Tensor, geom: GeometryCone3D, filter_kind: str, rank: int,

@@ -118,6 +118,34 @@ def fp_tensor(vol: torch.Tensor, geom, step: float, out: torch.Tensor | None = N
     raise TypeError(f"unsupported geometry {type(geom).__name__}")
 
 
+def fp_bands_tensor(vol: torch.Tensor, geom: GeometryCone3D, step: float, view_offset: int, dests,
+                    bands, pitch_rows: int) -> None:
+    """Forward projection of ``geom``'s views stored straight into row-band buffers
+    (tk_forward_cone_3d_bands): ray (v, r, c) goes to every destination h whose band
+    [r0_h, r1_h) holds row r, at ``dests[h][view_offset + v, r - r0_h, c]`` of a
+    (V_total, pitch_rows, cols) fp32 buffer.  ``dests`` are device addresses (ints) or
+    CUDA tensors -- peer addresses of other GPUs' buffers (CUDA IPC / symmetric memory)
+    make the stores the multi-GPU exchange itself."""
+    if not isinstance(geom, GeometryCone3D):
+        raise TypeError("band-routed forward projection is implemented for cone geometry")
+    if len(dests) != len(bands) or not 1 <= len(dests) <= 16:
+        raise ValueError("one band per destination, 1 to 16 destinations")
+    vol = _prep(vol, geom.volume_shape, "volume")
+    ptrs = [int(d.data_ptr()) if isinstance(d, torch.Tensor) else int(d) for d in dests]
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    r0 = (ctypes.c_int * len(bands))(*[int(b[0]) for b in bands])
+    r1 = (ctypes.c_int * len(bands))(*[int(b[1]) for b in bands])
+    src, minv = geom.ray_constants
+    (src, psrc), (minv, pminv) = _lib.host_f64(src), _lib.host_f64(minv)
+    nz, ny, nx = geom.volume_shape
+    sz, sy, sx = geom.volume_spacing
+    rows, cols = geom.detector_shape
+    with torch.cuda.device(vol.device):
+        _lib.call("tk_forward_cone_3d_bands", _lib.dev_ptr(vol), nz, ny, nx, sz, sy, sx, psrc, pminv,
+                  geom.n_projections, rows, cols, float(step), int(view_offset), len(ptrs), arr, r0, r1,
+                  int(pitch_rows), _lib.stream_ptr(vol.device))
+
+
 def forward_kernel_path(geom: GeometryCone3D) -> str:
     """Which cone forward kernel `fp_tensor` runs for this geometry (host-only
     query of tk_forward_cone_3d_path): "mirror" -- one thread marches a ray and
