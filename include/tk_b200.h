@@ -106,11 +106,13 @@ int tk_forward_cone_3d_bands(const float *vol, int nz, int ny, int nx, double sz
 int tk_forward_cone_3d_path(const double *sources, const double *minv, int n_views, int rows,
                             int cols, int nz, int ny, int nx);
 /* Forward-projection plan (no reference counterpart): the per-volume
- * preprocessing of tk_forward_cone_3d (zero-margin quad-tap copies of the
- * volume in two orientations) done once, then any number of view blocks
- * projected from it -- e.g. view chunks whose D2H copies overlap the next
- * chunk's kernel.  *plan is an opaque handle; destroy frees it stream-ordered
- * on `stream` (the caller orders other streams' uses before that). */
+ * preprocessing of tk_forward_cone_3d (the zero-margin, z-fastest coefficient
+ * cells of the volume) done once, then any number of view blocks projected from
+ * it -- e.g. view chunks whose D2H copies overlap the next chunk's kernel.  The
+ * cells are built on the first tk_fp_plan_project call, on that call's stream,
+ * from `vol`: the volume must stay allocated and unchanged until then.  *plan is
+ * an opaque handle; destroy frees it stream-ordered on `stream` (the caller
+ * orders other streams' uses before that). */
 int tk_fp_plan_create(const float *vol, int nz, int ny, int nx, double sz, double sy,
                       double sx, void **plan, void *stream);
 int tk_fp_plan_project(void *plan, const double *sources, const double *minv,
