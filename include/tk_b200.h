@@ -147,8 +147,9 @@ int tk_forward_cone_3d_adjoint(const float *sino, int n_views, int rows, int col
                                int nz, int ny, int nx, double sz, double sy,
                                double sx, double step, float *vol_out,
                                void *stream);
-/* As tk_forward_cone_3d_adjoint; deterministic = 1 accumulates in 64-bit fixed point
- * (scale 2^e from max |sino|, integer atomics): bit-reproducible, ~5x slower. */
+/* As tk_forward_cone_3d_adjoint; deterministic = 1 accumulates in fixed point with
+ * integer atomics (scale 2^e from a magnitude pass, the same scatter of |sino|; two
+ * components per 64-bit word): bit-reproducible, ~2.7x the fp32 time. */
 int tk_forward_cone_3d_adjoint_ex(const float *sino, int n_views, int rows, int cols,
                                   const double *sources, const double *minv, int nz, int ny,
                                   int nx, double sz, double sy, double sx, double step,

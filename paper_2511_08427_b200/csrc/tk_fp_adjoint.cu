@@ -8,9 +8,9 @@
 // and flushed as 16-byte vector reductions (REDG.E.ADD.F32x4, one per 4 taps)
 // into z-fastest tap quads; tiled folds sum the 4 quads holding each voxel's
 // tap back into the (z, y, x) volume.  fp32 atomics: summation order is not
-// deterministic.  Deterministic mode: 64-bit fixed-point quads with integer
-// atomics (associative: bit-reproducible), scale chosen from max |y| and a
-// geometric bound on the contributions per tap so no sum can overflow.
+// deterministic.  Deterministic mode: fixed-point quads with integer atomics
+// (associative: bit-reproducible), the scale chosen from a magnitude pass (the
+// same scatter of |y|) so no sum can overflow; two components per 64-bit word.
 //
 // Bound: the L2 vector-reduction pipeline (cfg5: 2.0e11 reduction sectors, atomic input
 // 59 % busy, half the sectors miss L2).  Measured at cfg5 (profiles/r02): pair arithmetic
@@ -41,17 +41,26 @@ constexpr int kFpzRows = 8;  // detector rows per quarter-warp (one column)
 // registers and only the row left behind is flushed (one REDG.F32x4 instead of
 // two).
 // DET: fixed-point flush -- each quad component is rounded to an integer multiple of
-// 2^-e (scale = 2^e, exact) and added with 64-bit integer atomics into u64 quads.
-// Integer addition is associative, so the result does not depend on the order in
-// which rays flush: bit-reproducible (torch.use_deterministic_algorithms).
+// 2^-e (scale = 2^e, exact) and added with 64-bit integer atomics.  Integer addition is
+// associative, so the result does not depend on the order in which rays flush:
+// bit-reproducible (torch.use_deterministic_algorithms).  Two components share one
+// 64-bit word, a + 2^32 b: e is chosen so every component's total stays below 2^30 in
+// magnitude, so the low 32 bits of the word, read as a signed int, are exactly sum(a)
+// and (word - sum(a)) / 2^32 is exactly sum(b) -- two atomics per quad instead of four.
+__device__ __forceinline__ unsigned long long fx_pack(float a, float b, float scale) {
+  return (unsigned long long)((long long)__float2int_rn(a * scale) + ((long long)__float2int_rn(b * scale) << 32));
+}
 __device__ __forceinline__ void red_add_fx4(unsigned long long *p, const float4 &v, float scale) {
-  atomicAdd(p, (unsigned long long)__float2ll_rn(v.x * scale));
-  atomicAdd(p + 1, (unsigned long long)__float2ll_rn(v.y * scale));
-  atomicAdd(p + 2, (unsigned long long)__float2ll_rn(v.z * scale));
-  atomicAdd(p + 3, (unsigned long long)__float2ll_rn(v.w * scale));
+  atomicAdd(p, fx_pack(v.x, v.y, scale));
+  atomicAdd(p + 1, fx_pack(v.z, v.w, scale));
+}
+__device__ __forceinline__ long long fx_unpack(unsigned long long w, int half) {
+  const long long lo = (long long)(int)(unsigned)w;  // sign-extended low component
+  return half ? ((long long)w - lo) >> 32 : lo;
 }
 
-template <int MINB, bool DET = false, bool CARRY = true>
+// ABS: scatter |y| (fp32) -- the deterministic mode's magnitude pass (launch_fp_adjoint_det).
+template <int MINB, bool DET = false, bool CARRY = true, bool ABS = false>
 __global__ void __launch_bounds__(128, MINB)
     cone_fp_adjoint4z_kernel(const float *__restrict__ sino, void *__restrict__ qy_, void *__restrict__ qx_,
                              int nx, int ny, int nz, double sx, double sy, double sz,
@@ -68,7 +77,8 @@ __global__ void __launch_bounds__(128, MINB)
   const int c = cb * kCols + warp * 4 + (lane >> 3);
   const int r = rb * kFpzRows + (lane & 7);
   if (c >= cols || r >= rows) return;
-  const float y = __ldg(sino + ((long long)v * rows + r) * cols + c);
+  const float y = ABS ? fabsf(__ldg(sino + ((long long)v * rows + r) * cols + c))
+                      : __ldg(sino + ((long long)v * rows + r) * cols + c);
   if (y == 0.f) return;
   RaySetup rs;
   if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) return;
@@ -96,7 +106,7 @@ __global__ void __launch_bounds__(128, MINB)
     const float2 a = upk2(q01), c = upk2(q23);
     const float4 v = make_float4(a.x, a.y, c.x, c.y);
     if (DET)
-      red_add_fx4(static_cast<unsigned long long *>(qv) + 4ull * cidx, v, scale);
+      red_add_fx4(static_cast<unsigned long long *>(qv) + 2ull * cidx, v, scale);
     else
       red_add_v4(static_cast<float4 *>(qv) + cidx, v);
   };
@@ -157,9 +167,14 @@ __global__ void __launch_bounds__(256) unquad_fx_kernel(const unsigned long long
     const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long long)nx * ny));
     const long long zp = z + m, yp = y + m, xp = x + m;
     // qy: Qz[y][x][z] taps (z,x),(z,x+1),(z+1,x),(z+1,x+1) of row y
-    auto Y = [&](long long yy, long long xx, long long zz, int c) { return (long long)qy[4 * ((yy * px + xx) * pz + zz) + c]; };
+    // (two packed components per 64-bit word: fx_unpack)
+    auto Y = [&](long long yy, long long xx, long long zz, int c) {
+      return fx_unpack(qy[2 * ((yy * px + xx) * pz + zz) + (c >> 1)], c & 1);
+    };
     // qx: Qx[x][y][z] taps (z,y),(z,y+1),(z+1,y),(z+1,y+1) of row x
-    auto X = [&](long long xx, long long yy, long long zz, int c) { return (long long)qx[4 * ((xx * py + yy) * pz + zz) + c]; };
+    auto X = [&](long long xx, long long yy, long long zz, int c) {
+      return fx_unpack(qx[2 * ((xx * py + yy) * pz + zz) + (c >> 1)], c & 1);
+    };
     const long long t = Y(yp, xp, zp, 0) + Y(yp, xp - 1, zp, 1) + Y(yp, xp, zp - 1, 2) + Y(yp, xp - 1, zp - 1, 3) +
                         X(xp, yp, zp, 0) + X(xp, yp - 1, zp, 1) + X(xp, yp, zp - 1, 2) + X(xp, yp - 1, zp - 1, 3);
     vol[i] = (float)((double)t * inv_scale);
@@ -235,93 +250,49 @@ __global__ void __launch_bounds__(256) unquad_z_kernel(const float4 *__restrict_
 }
 
 
-// Upper bound on the number of step-sized contributions one voxel tap can
-// receive over all views of a forward-projection transpose: per view, the rays
-// that can pass within the tap's support (a ball of radius rho = sqrt(3) s_max
-// around it) times the samples each such ray places in it.  Rays diverge from
-// the source, so at distance >= dmin (source to the volume box) adjacent
-// pixels' rays are >= dmin * alpha apart, alpha = the smallest angle between
-// adjacent pixels' rays, attained at a detector corner for a flat detector
-// (halved for safety).  Returns +inf when a source lies inside the box.
-static double fp_adjoint_tap_count_bound(const double *sources, const double *minv, int n_views, int rows, int cols,
-                                         int nz, int ny, int nx, double sz, double sy, double sx, double step) {
-  const double h[3] = {(nx + 1) * sx / 2.0, (ny + 1) * sy / 2.0, (nz + 1) * sz / 2.0};
-  const double rho = std::sqrt(3.0) * std::max(sx, std::max(sy, sz));
-  const double samples = 2.0 * rho / step + 2.0;
-  double total = 0.0;
-  for (int i = 0; i < n_views; ++i) {
-    const double *s = sources + 3 * i, *m = minv + 9 * i;
-    double d2 = 0.0;
-    for (int k = 0; k < 3; ++k) {
-      const double e = std::max(0.0, std::fabs(s[k]) - h[k]);
-      d2 += e * e;
-    }
-    const double dmin = std::sqrt(d2);
-    if (!(dmin > 0.0)) return INFINITY;
-    auto dir = [&](double c, double r, double out[3]) {
-      for (int k = 0; k < 3; ++k) out[k] = m[3 * k] * c + m[3 * k + 1] * r + m[3 * k + 2];
-      const double n = std::sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
-      for (int k = 0; k < 3; ++k) out[k] /= n;
-    };
-    auto angle = [](const double a[3], const double b[3]) {
-      const double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
-      return std::atan2(std::sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
-    };
-    double au = INFINITY, av = INFINITY;
-    for (int cc = 0; cc < 2; ++cc)
-      for (int rr = 0; rr < 2; ++rr) {
-        const double c = cc ? cols - 1 : 0, r = rr ? rows - 1 : 0;
-        double d[3], du[3], dv[3];
-        dir(c, r, d);
-        dir(c + (cc ? -1 : 1), r, du);
-        dir(c, r + (rr ? -1 : 1), dv);
-        au = std::min(au, angle(d, du));
-        av = std::min(av, angle(d, dv));
-      }
-    au *= 0.5;
-    av *= 0.5;
-    const double nu = cols > 1 ? 2.0 * rho / (dmin * au) + 2.0 : 1.0;
-    const double nv = rows > 1 ? 2.0 * rho / (dmin * av) + 2.0 : 1.0;
-    total += nu * nv * samples;
-  }
-  return total;
-}
-
-// Deterministic A^T: fixed-point scale 2^e from max |y| and the geometry's tap
-// contribution bound, so that no tap sum can overflow int64 (each contribution
-// <= |y| step).
+// Deterministic A^T.  Pass 1 scatters |y| in fp32 into the same quad cells: the largest
+// component, doubled (fp32 rounding of a sum of non-negative terms is far below that), bounds
+// every component total of the real scatter in magnitude.  The fixed-point scale 2^e keeps
+// those totals below 2^30, so two components share each 64-bit atomic word (fx_pack): pass 2
+// scatters y in fixed point with two integer atomics per quad, and the fold sums integers.
+// The data-driven bound leaves ~30 bits for the largest tap (a geometric bound on the
+// contributions per tap was ~1000x looser and cost the fixed point 5e-5 relative accuracy).
 static int launch_fp_adjoint_det(const float *sino, int nz, int ny, int nx, double sz, double sy, double sx,
-                                 Scratch &dviews, int n_views, int rows, int cols,
-                                 double step, double tap_count, float *vol, cudaStream_t st) {
+                                 Scratch &dviews, int n_views, int rows, int cols, double step, float *vol,
+                                 cudaStream_t st) {
   constexpr int m2 = 2 * kFpMargin;
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
-  const long long nsino = (long long)n_views * rows * cols;
   Scratch dmax, qA, qB;
+  TK_TRY_CUDA(qA.alloc(16 * ncell, st));
+  TK_TRY_CUDA(qB.alloc(16 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, 16 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, 16 * ncell, st));
+  const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
+  if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  cone_fp_adjoint4z_kernel<8, false, true, true><<<(unsigned)nbz, 128, 0, st>>>(
+      sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz, dviews.as<ConeRayView>(), rows, cols, n_views, step, 1.f);
+  TK_LAUNCHED("cone_fp_adjoint4z_kernel");
   TK_TRY_CUDA(dmax.alloc(sizeof(unsigned), st));
   TK_TRY_CUDA(cudaMemsetAsync(dmax.ptr, 0, sizeof(unsigned), st));
-  absmax_kernel<<<(unsigned)std::min<long long>(ceil_div(nsino, 256), (long long)sm_count() * 8), 256, 0, st>>>(
-      sino, nsino, dmax.as<unsigned>());
+  const unsigned mg = (unsigned)std::min<long long>(ceil_div(4 * ncell, 256), (long long)sm_count() * 8);
+  absmax_kernel<<<mg, 256, 0, st>>>(qA.as<float>(), 4 * ncell, dmax.as<unsigned>());
+  TK_LAUNCHED("absmax_kernel");
+  absmax_kernel<<<mg, 256, 0, st>>>(qB.as<float>(), 4 * ncell, dmax.as<unsigned>());
   TK_LAUNCHED("absmax_kernel");
   unsigned bits = 0;
   TK_TRY_CUDA(cudaMemcpyAsync(&bits, dmax.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   TK_TRY_CUDA(cudaStreamSynchronize(st));
-  float ymax;
-  std::memcpy(&ymax, &bits, sizeof(float));
-  if (!(ymax > 0.f) || !std::isfinite(ymax)) {
+  float amax;
+  std::memcpy(&amax, &bits, sizeof(float));
+  if (!std::isfinite(amax)) return fail_arg("tk_forward_cone_3d_adjoint: non-finite sinogram");
+  if (!(amax > 0.f)) {
     TK_TRY_CUDA(cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nz * ny * nx, st));
-    return std::isfinite(ymax) ? TK_OK : fail_arg("tk_forward_cone_3d_adjoint: non-finite sinogram");
+    return TK_OK;
   }
-  if (!std::isfinite(tap_count))
-    return fail_arg("tk_forward_cone_3d_adjoint: deterministic mode needs every source outside the volume");
-  const double bound = (double)ymax * step * tap_count;
-  const int e = std::min(100, (int)std::floor(62.0 - std::log2(bound)));
+  const int e = std::min(100, (int)std::floor(30.0 - std::log2(2.0 * (double)amax)));
   const float scale = std::ldexp(1.0f, e);
-  TK_TRY_CUDA(qA.alloc(32 * ncell, st));
-  TK_TRY_CUDA(qB.alloc(32 * ncell, st));
-  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, 32 * ncell, st));
-  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, 32 * ncell, st));
-  const long long nbz = (long long)ceil_div(cols, 16) * ceil_div(rows, kFpzRows) * n_views;
-  if (nbz >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_adjoint: problem too large for one launch");
+  TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, 16 * ncell, st));
+  TK_TRY_CUDA(cudaMemsetAsync(qB.ptr, 0, 16 * ncell, st));
   cone_fp_adjoint4z_kernel<8, true><<<(unsigned)nbz, 128, 0, st>>>(sino, qA.ptr, qB.ptr, nx, ny, nz, sx, sy, sz,
                                                                    dviews.as<ConeRayView>(), rows, cols, n_views, step,
                                                                    scale);
@@ -347,10 +318,7 @@ static int launch_fp_adjoint(const float *sino, int nz, int ny, int nx, double s
   const long long ncell = (long long)(nz + m2) * (ny + m2) * (nx + m2);
   if (ncell >= (1LL << 32)) return fail_arg("tk_forward_cone_3d_adjoint: volume too large for 32-bit cell indices");
   if (deterministic)
-    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, dviews, n_views, rows, cols, step,
-                                 fp_adjoint_tap_count_bound(sources, minv, n_views, rows, cols, nz, ny, nx, sz, sy,
-                                                            sx, step),
-                                 vol, st);
+    return launch_fp_adjoint_det(sino, nz, ny, nx, sz, sy, sx, dviews, n_views, rows, cols, step, vol, st);
   TK_TRY_CUDA(qA.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(qB.alloc(sizeof(float4) * ncell, st));
   TK_TRY_CUDA(cudaMemsetAsync(qA.ptr, 0, sizeof(float4) * ncell, st));
