@@ -30,7 +30,7 @@ namespace tk {
 constexpr int kFpzRows = 8;  // detector rows per quarter-warp (one column)
 
 
-// z-fastest form of the quad scatter (the transpose of cone_fp4z_kernel, "red4z",
+// z-fastest form of the quad scatter (the transpose of cone_fp_kernel, tk_fp.cu,
 // default): quarter = 8 rows of one column, so lanes flush together into
 // contiguous quads.  Two scatter buffers, one per horizontal row axis b:
 //   qy: Qz[y][x][z] += (w(z,x), w(z,x+1), w(z+1,x), w(z+1,x+1)) of row y,

@@ -1,6 +1,7 @@
-"""Time the forward / back projector algorithm variants at cfg4 and report
-their accuracy against the float32 LDG kernel (and, for a view subset, the
-float64 oracle when --oracle is given).
+"""Time the forward / back projector kernel variants at cfg4 -- the default kernels
+against the measured comparisons the north star asks for (texture unit, the
+warp-cooperative march, the general-P quad back projector) -- and report each
+result's relative L2 difference from the first one listed.
 
     python scripts/bench_variants.py [--views 720] [--reps 3] [--out gpurun_out/variants.json]
 """
@@ -24,8 +25,8 @@ from paper_2511_08427_b200.projectors import bp_tensor, fp_tensor  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--views", type=int, default=720)
 ap.add_argument("--reps", type=int, default=3)
-ap.add_argument("--fp", default="ldg2,ldg,tex,hwtex")
-ap.add_argument("--bp", default="quad,ldg,tex,hwtex")
+ap.add_argument("--fp", default="default,warp,tex,hwtex")
+ap.add_argument("--bp", default="tma,quad,tex,hwtex")
 ap.add_argument("--out", default="")
 a = ap.parse_args()
 
@@ -67,7 +68,7 @@ for algo in a.fp.split(","):
         ref_sino = sino.clone()
     res["fp"][algo] = {"ms": round(ms, 3), "gups": round(nvox * V / ms / 1e6, 2), "rel_vs_first": rel(sino, ref_sino)}
     print("fp", algo, res["fp"][algo], flush=True)
-os.environ["TK_FP_ALGO"] = "tex"
+os.environ.pop("TK_FP_ALGO", None)
 
 filt = filter_stage_tensor(ref_sino, geom, "shepp_logan")
 out = torch.empty(geom.volume_shape, device="cuda")

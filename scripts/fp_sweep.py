@@ -1,6 +1,7 @@
 """Sweep environment-selected kernel configurations of one operator at cfg4.
 
-    python scripts/fp_sweep.py --op fp --configs "TK_FP2_RAYS=1,TK_FP2_MINB=10;TK_FP2_RAYS=2,TK_FP2_MINB=6"
+    python scripts/fp_sweep.py --op fp --configs "TK_FP_MIRROR=0;TK_FP_MIRROR=1,TK_FP_CFG=6x2"
+    python scripts/fp_sweep.py --op bp --configs "TK_BP_ALGO=tma;TK_BP_ALGO=quad"
 """
 
 import argparse
