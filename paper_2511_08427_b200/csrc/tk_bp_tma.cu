@@ -6,18 +6,19 @@
 // data pipe -- every 16-byte quad load costs one wavefront per 128-byte line
 // touched by each quarter-warp (~1.4 lines per quarter at cfg4, ncu), and the
 // quad layout itself is a 12 GB expansion written every call.  Here
-//   * a CTA owns a 16 x 16 x 16 voxel block; for every view a producer warp
+//   * a CTA owns a 16 x 16 x 32 voxel block; for every view a producer warp
 //     projects the block's 8 corners (exact bound of a central projection of a
 //     convex box), and one elected lane issues ONE 3D TMA copy of the covering
-//     detector rectangle [r0, r0 + bh) x [c0, c0 + bw) of that view (c0 a
+//     detector rectangle [r0, r0 + bh) x [c0, c0 + BW) of that view (c0 a
 //     multiple of 4: TMA box starts must be 16-byte aligned) into a
 //     shared-memory stage (out-of-detector texels are zero-filled by the TMA
 //     unit: the reference's per-tap zero extension, _kernels.py:308-317);
-//   * an 8-stage mbarrier ring (full: TMA bytes landed, empty: the 8 consumer
-//     warps are done) keeps 7 views in flight while 256 consumer threads
-//     (one (x, y) column and 16 z-voxels each) gather the 4 bilinear taps of
-//     every update with scalar LDS -- one data-pipe wavefront per warp and tap,
-//     conflict-light because a warp's footprint is ~20 consecutive columns;
+//   * an mbarrier ring of up to 8 stages (as many as fit two CTAs per SM: 6 at
+//     cfg4; full: TMA bytes landed, empty: all 256 consumer threads released)
+//     keeps the next views in flight while the consumers (one (x, y) column and
+//     32 z-voxels each) gather the 4 bilinear taps of every update with scalar
+//     LDS at immediate offsets -- one data-pipe wavefront per warp and tap, the
+//     tile pitch BW == 12 or 20 (mod 32) keeping a warp's rows in disjoint banks;
 //   * column, depth and (sid/w)^2 are computed once per (column, view); only the
 //     row advances along z; floors use floor_magic (no conversion-pipe ops).
 // A (block, view) whose rectangle exceeds the TMA box (extreme magnification)
