@@ -25,6 +25,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running full-size case")
 
 
+@pytest.fixture(autouse=True)
+def _seed_torch():
+    # unseeded torch draws in a test are then the same whatever ran before it
+    try:
+        import torch
+
+        torch.manual_seed(0)
+    except ImportError:  # pragma: no cover
+        pass
+
+
 @pytest.fixture()
 def rng():
     # the reference suite's seed (pkg/tests/conftest.py:18-20)
