@@ -238,7 +238,7 @@ def ncu_traffic(kernel: str):
             continue
         k = d.get(kernel) or {}
         if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
-            return float(k["dram_bytes_per_launch"]), f"profiles/{p.name}"
+            return float(k["dram_bytes_per_launch"]), str(p.relative_to(ROOT))
     return None, None
 
 
