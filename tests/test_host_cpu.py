@@ -226,12 +226,18 @@ def test_tapered_pipeline_chunks_cover_views_once():
         for parts in (1, 3, 12):
             for small in (0, 1, 8, 12):
                 for head in (True, False):
-                    ch = _tapered(n, parts, small, head)
-                    assert ch[0][0] == 0 and ch[-1][1] == n
-                    assert all(b < e for b, e in ch) and all(ch[i][1] == ch[i + 1][0] for i in range(len(ch) - 1))
-                    if n > max(1, small):
-                        short = ch[0] if head else ch[-1]
-                        assert short[1] - short[0] == max(1, small)
+                    for align in (1, 8):
+                        ch = _tapered(n, parts, small, head, align)
+                        assert ch[0][0] == 0 and ch[-1][1] == n
+                        assert all(b < e for b, e in ch)
+                        assert all(ch[i][1] == ch[i + 1][0] for i in range(len(ch) - 1))
+                        want = -(-max(1, small) // align) * align
+                        if n > want:
+                            short = ch[0] if head else ch[-1]
+                            assert short[1] - short[0] == want
+                            # every other chunk but the one before the short tail is aligned
+                            body = ch[1:] if head else ch[:-1]
+                            assert all((e - b) % align == 0 for b, e in body[:-1])
 
 
 def test_bp_tile_bank_model_supports_the_8x4_warp_and_pitch_rule():
