@@ -177,10 +177,13 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     if (s == kBtStages) s = 0, fph ^= 1u;
     mbar_wait(&full[s], fph);
     const BtMeta m = meta[s];
-    const ConeVoxView &V = p.views[v];  // uniform across the CTA: L1 broadcast (measured faster than a smem copy)
-    const float a0 = fmaf(V.a[0], xc, fmaf(V.a[1], yc, fmaf(V.a[2], zc0, V.a[3])));
-    const float b0 = fmaf(V.b[0], xc, fmaf(V.b[1], yc, fmaf(V.b[2], zc0, V.b[3])));
-    const float w0 = fmaf(V.w[0], xc, fmaf(V.w[1], yc, fmaf(V.w[2], zc0, V.w[3])));
+    // the view's constants, uniform across the CTA: three 16-byte L1 broadcasts (as 12
+    // scalar loads they were 8 % of the L1 data pipe's wavefronts)
+    const float4 *vp = reinterpret_cast<const float4 *>(p.views + v);
+    const float4 va = __ldg(vp), vb = __ldg(vp + 1), vw = __ldg(vp + 2);
+    const float a0 = fmaf(va.x, xc, fmaf(va.y, yc, fmaf(va.z, zc0, va.w)));
+    const float b0 = fmaf(vb.x, xc, fmaf(vb.y, yc, fmaf(vb.z, zc0, vb.w)));
+    const float w0 = fmaf(vw.x, xc, fmaf(vw.y, yc, fmaf(vw.z, zc0, vw.w)));
     if (active && w0 > (float)kTiny) {  // _kernels.py:297-298
       float rw;  // MUFU.RCP (rel. error 2^-23), one instruction instead of the IEEE division sequence
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"(w0));
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
       }
       const float g0 = q * (1.f - wc), g1 = q * wc;
       const float fr0 = fmaf(b0, rw, p.cv);
-      const float dr = V.b[2] * rw;
+      const float dr = vb.z * rw;
       if (m.fits) {
         // byte address of tap (row bits, c0) = row_bits * 4 BW + vbase (mod 2^32): the
         // FADD.RM floor's float bits ARE kFloorBits + row
