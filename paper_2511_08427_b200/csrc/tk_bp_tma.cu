@@ -45,6 +45,14 @@ struct BtMeta {
   int c0, r0, fits, pad;
 };
 
+// The views of one launch travel in the kernel's parameter block (constant bank):
+// the per-view constants are then uniform constant loads, off the L1 data pipe the
+// tile gathers saturate.  Longer scans are launched in blocks of views.
+constexpr int kBtParamViews = 640;
+struct BtViews {
+  float4 q[3 * kBtParamViews];  // (a, b, w) of view v at q[3 v .. 3 v + 2]
+};
+
 // ZB = 32 z-voxels per thread (halves the per-view set-up per update against 16);
 // BW = the tile row pitch (floats) = the TMA box width, a compile-time constant so a
 // voxel's two tile rows are ONE IMAD (row bits x 4 BW + per-view base) and four LDS
@@ -65,7 +73,7 @@ __device__ __forceinline__ float lds_off(unsigned a) {
 template <int BW>
 __global__ void __launch_bounds__(kBtThreads, 2)
     cone_bp_tma_kernel(const __grid_constant__ CUtensorMap map, const BpParams p, int weighted, int bh,
-                       int stage_floats, int nst, unsigned fbias) {
+                       int stage_floats, int nst, unsigned fbias, int v_base, const __grid_constant__ BtViews pv) {
   constexpr int kBtZB = 32, bw = BW;
   const int kBtStages = nst;
   extern __shared__ float bt_raw[];  // [kBtStages][stage_floats] at a 128-byte aligned base
@@ -101,16 +109,16 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     for (int v = 0; v < p.n_views; ++v, ++s) {
       if (s == kBtStages) s = 0, eph ^= 1u;
       if (v >= kBtStages) mbar_wait(&empty[s], eph);
-      const ConeVoxView &V = p.views[v];
+      const float4 va = pv.q[3 * v], vb = pv.q[3 * v + 1], vw = pv.q[3 * v + 2];
       float cmin = 3e38f, cmax = -3e38f, rmin = 3e38f, rmax = -3e38f;
       bool behind = false;
       if (lane < 8) {
         const float x = (lane & 1) ? bx1 : bx0, y = (lane & 2) ? by1 : by0, z = (lane & 4) ? bz1 : bz0;
-        const float w = fmaf(V.w[0], x, fmaf(V.w[1], y, fmaf(V.w[2], z, V.w[3])));
+        const float w = fmaf(vw.x, x, fmaf(vw.y, y, fmaf(vw.z, z, vw.w)));
         behind = !(w > (float)kTiny);
         const float rw = 1.f / w;
-        const float fc = fmaf(fmaf(V.a[0], x, fmaf(V.a[1], y, fmaf(V.a[2], z, V.a[3]))), rw, p.cu);
-        const float fr = fmaf(fmaf(V.b[0], x, fmaf(V.b[1], y, fmaf(V.b[2], z, V.b[3]))), rw, p.cv);
+        const float fc = fmaf(fmaf(va.x, x, fmaf(va.y, y, fmaf(va.z, z, va.w))), rw, p.cu);
+        const float fr = fmaf(fmaf(vb.x, x, fmaf(vb.y, y, fmaf(vb.z, z, vb.w))), rw, p.cv);
         cmin = cmax = fc;
         rmin = rmax = fr;
       }
@@ -136,7 +144,7 @@ __global__ void __launch_bounds__(kBtThreads, 2)
         meta[s] = m;
         if (fits) {
           mbar_arrive_tx(&full[s], tx_bytes);
-          tma_load_3d(bt_tiles + (size_t)s * stage_floats, &map, m.c0, m.r0, v, &full[s]);
+          tma_load_3d(bt_tiles + (size_t)s * stage_floats, &map, m.c0, m.r0, v_base + v, &full[s]);
         } else {
           mbar_arrive(&full[s]);
         }
@@ -177,10 +185,9 @@ __global__ void __launch_bounds__(kBtThreads, 2)
     if (s == kBtStages) s = 0, fph ^= 1u;
     mbar_wait(&full[s], fph);
     const BtMeta m = meta[s];
-    // the view's constants, uniform across the CTA: three 16-byte L1 broadcasts (as 12
-    // scalar loads they were 8 % of the L1 data pipe's wavefronts)
-    const float4 *vp = reinterpret_cast<const float4 *>(p.views + v);
-    const float4 va = __ldg(vp), vb = __ldg(vp + 1), vw = __ldg(vp + 2);
+    // the view's constants: uniform constant-bank loads (as 12 scalar global loads they
+    // were 8 % of the L1 data pipe's wavefronts, as three 16-byte broadcasts ~2 %)
+    const float4 va = pv.q[3 * v], vb = pv.q[3 * v + 1], vw = pv.q[3 * v + 2];
     const float a0 = fmaf(va.x, xc, fmaf(va.y, yc, fmaf(va.z, zc0, va.w)));
     const float b0 = fmaf(vb.x, xc, fmaf(vb.y, yc, fmaf(vb.z, zc0, vb.w)));
     const float w0 = fmaf(vw.x, xc, fmaf(vw.y, yc, fmaf(vw.z, zc0, vw.w)));
@@ -327,15 +334,27 @@ static void footprint_box(const BpParams &p, const ConeVoxView *hv, int kBtZB, i
 // Tile pitches: the TMA box width, == 12 or 20 (mod 32) so that an 8 x 4 warp's taps on
 // neighbouring tile rows fall in disjoint banks (scripts/bp_bank_model.py).
 template <int BW>
-static int launch_bp_tma_t(const BpParams &p, const CUtensorMap &map, bool weighted, int bh, int stage_floats, int nst,
-                           cudaStream_t st) {
+static int launch_bp_tma_t(const BpParams &p, const ConeVoxView *host_views, const CUtensorMap &map, bool weighted,
+                           int bh, int stage_floats, int nst, cudaStream_t st) {
   const size_t smem = sizeof(float) * (size_t)stage_floats * nst + 128;
   auto kern = cone_bp_tma_kernel<BW>;
   TK_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((p.nx + kBtTX - 1) / kBtTX, (p.ny + kBtTY - 1) / kBtTY, (p.z_count + 31) / 32);
-  kern<<<grid, kBtThreads, smem, st>>>(map, p, weighted ? 1 : 0, bh, stage_floats, nst,
-                                       kFloorBits * (4u * BW) + 4u * kFloorBits);
-  TK_LAUNCHED("cone_bp_tma_kernel");
+  static thread_local BtViews pv;
+  const int nblk = (p.n_views + kBtParamViews - 1) / kBtParamViews;
+  const int per = (p.n_views + nblk - 1) / nblk;  // equal blocks: each launch refills its ring once
+  for (int v0 = 0; v0 < p.n_views; v0 += per) {
+    const int cnt = std::min(per, p.n_views - v0);
+    BpParams pb = p;
+    pb.n_views = cnt;
+    pb.sino = p.sino + (long long)v0 * p.view_stride;
+    pb.views = p.views + v0;
+    pb.accumulate = p.accumulate || v0 > 0;
+    std::memcpy(pv.q, host_views + v0, sizeof(ConeVoxView) * cnt);
+    kern<<<grid, kBtThreads, smem, st>>>(map, pb, weighted ? 1 : 0, bh, stage_floats, nst,
+                                         kFloorBits * (4u * BW) + 4u * kFloorBits, v0, pv);
+    TK_LAUNCHED("cone_bp_tma_kernel");
+  }
   return TK_OK;
 }
 
@@ -371,20 +390,20 @@ int launch_bp_tma(const BpParams &p, const ConeVoxView *host_views, bool weighte
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -1;
   switch (bw) {
-    case 44: return launch_bp_tma_t<44>(p, map, weighted, bh, stage_floats, nst, st);
-    case 52: return launch_bp_tma_t<52>(p, map, weighted, bh, stage_floats, nst, st);
-    case 76: return launch_bp_tma_t<76>(p, map, weighted, bh, stage_floats, nst, st);
-    case 84: return launch_bp_tma_t<84>(p, map, weighted, bh, stage_floats, nst, st);
-    case 108: return launch_bp_tma_t<108>(p, map, weighted, bh, stage_floats, nst, st);
-    case 116: return launch_bp_tma_t<116>(p, map, weighted, bh, stage_floats, nst, st);
-    case 140: return launch_bp_tma_t<140>(p, map, weighted, bh, stage_floats, nst, st);
-    case 148: return launch_bp_tma_t<148>(p, map, weighted, bh, stage_floats, nst, st);
-    case 172: return launch_bp_tma_t<172>(p, map, weighted, bh, stage_floats, nst, st);
-    case 180: return launch_bp_tma_t<180>(p, map, weighted, bh, stage_floats, nst, st);
-    case 204: return launch_bp_tma_t<204>(p, map, weighted, bh, stage_floats, nst, st);
-    case 212: return launch_bp_tma_t<212>(p, map, weighted, bh, stage_floats, nst, st);
-    case 236: return launch_bp_tma_t<236>(p, map, weighted, bh, stage_floats, nst, st);
-    default: return launch_bp_tma_t<244>(p, map, weighted, bh, stage_floats, nst, st);
+    case 44: return launch_bp_tma_t<44>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 52: return launch_bp_tma_t<52>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 76: return launch_bp_tma_t<76>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 84: return launch_bp_tma_t<84>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 108: return launch_bp_tma_t<108>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 116: return launch_bp_tma_t<116>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 140: return launch_bp_tma_t<140>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 148: return launch_bp_tma_t<148>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 172: return launch_bp_tma_t<172>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 180: return launch_bp_tma_t<180>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 204: return launch_bp_tma_t<204>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 212: return launch_bp_tma_t<212>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    case 236: return launch_bp_tma_t<236>(p, host_views, map, weighted, bh, stage_floats, nst, st);
+    default: return launch_bp_tma_t<244>(p, host_views, map, weighted, bh, stage_floats, nst, st);
   }
 }
 
