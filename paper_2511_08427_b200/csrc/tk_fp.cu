@@ -166,7 +166,7 @@ struct FpDests {
   long long view_stride;
 };
 
-template <int VG, bool FIXS, bool BANDS, int PIPE = 0>
+template <int VG, bool FIXS, bool BANDS>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
@@ -227,132 +227,18 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   float acc = 0.f;
   float kf = 0.5f;
   const int nfull = rs.n - 1;
-  if (PIPE == 2) {
-    // Two-deep pipeline: cells of samples k + 1 (b) and k + 2 (the load target a) in
-    // flight while sample k is interpolated; a keeps b's data when the cell repeats.
-    const float klast = (float)nfull + 0.5f * rs.last;
-    auto locate = [&](float kk, unsigned &id, float2 &w, float &wz) {
-      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
-      const float fz = fmaf(kk, gz, ez);
-      const unsigned long long xxy = fadd2_rm(fxy, m2);
-      const float xz = __fadd_rd(fz, magic);
-      const float2 xb = upk2(xxy);
-      id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
-      w = upk2(fsub2(fxy, fsub2(xxy, m2)));
-      wz = fz - (xz - magic);
-    };
-    auto interp = [&](const float4 &l, const float4 &h, float2 w, float wz) -> float {
-      const float2 tl = upk2(ffma2(pk2(l.z, l.w), pk2(w.x, w.x), pk2(l.x, l.y)));
-      const float2 th = upk2(ffma2(pk2(h.z, h.w), pk2(w.x, w.x), pk2(h.x, h.y)));
-      const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
-      return lerpf(s0, s1, w.y);
-    };
-    auto kk_of = [&](int j) { return j < nfull ? (float)j + 0.5f : klast; };
-    const int n = rs.n;
-    float2 w0, w1;
-    float wz0, wz1;
-    unsigned id0, id1;
-    float4 l0, h0, l1, h1;
-    locate(kk_of(0), id0, w0, wz0);
-    {
-      const float4 *p = elem_ptr(q, id0);
-      l0 = __ldg(p);
-      h0 = __ldg(p + sys);
-    }
-    locate(kk_of(1), id1, w1, wz1);  // harmless past the end (n == 1): never interpolated
-    if (id1 != id0) {
-      const float4 *p = elem_ptr(q, id1);
-      l1 = __ldg(p);
-      h1 = __ldg(p + sys);
-    } else {
-      l1 = l0, h1 = h0;
-    }
-    for (int k = 0; k < n; ++k) {
-      unsigned id2;
-      float2 w2;
-      float wz2;
-      locate(kk_of(k + 2), id2, w2, wz2);
-      const float val = interp(l0, h0, w0, wz0);
-      acc = k < nfull ? acc + val : fmaf(rs.last, val, acc);
-      if (id2 != id1) {
-        const float4 *p = elem_ptr(q, id2);
-        l0 = __ldg(p);
-        h0 = __ldg(p + sys);
-      } else {
-        l0 = l1, h0 = h1;
-      }
-      // rotate: (l0, h0) <-> (l1, h1) by swapping names
-      const float4 tl = l0, th = h0;
-      l0 = l1, h0 = h1, l1 = tl, h1 = th;
-      w0 = w1, wz0 = wz1, w1 = w2, wz1 = wz2, id1 = id2;
-    }
-    store(acc * (float)step);
-    return;
-  }
-  if (PIPE == 1) {
-    // Software-pipelined march (same samples, cells and arithmetic): the position,
-    // weights and cell of sample k + 1 are computed before sample k is interpolated,
-    // and sample k + 1's cell is loaded (on a cell change) right after sample k's
-    // interpolation has read the registers it overwrites -- the load is in flight
-    // while sample k + 2's set-up runs.
-    const float klast = (float)nfull + 0.5f * rs.last;
-    auto locate = [&](float kk, unsigned &id, float2 &w, float &wz) {
-      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
-      const float fz = fmaf(kk, gz, ez);
-      const unsigned long long xxy = fadd2_rm(fxy, m2);
-      const float xz = __fadd_rd(fz, magic);
-      const float2 xb = upk2(xxy);
-      id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
-      w = upk2(fsub2(fxy, fsub2(xxy, m2)));
-      wz = fz - (xz - magic);
-    };
-    auto interp = [&](float2 w, float wz) -> float {
-      const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
-      const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
-      const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
-      return lerpf(s0, s1, w.y);
-    };
-    float2 w;
-    float wz;
-    locate(nfull > 0 ? kf : klast, cell, w, wz);
-    {
-      const float4 *p = elem_ptr(q, cell);
-      lo4 = __ldg(p);
-      hi4 = __ldg(p + sys);
-    }
-#pragma unroll 2
-    for (int k = 0; k < nfull; ++k, kf += 1.f) {
-      unsigned id1;
-      float2 w1;
-      float wz1;
-      locate(k + 1 < nfull ? kf + 1.f : klast, id1, w1, wz1);
-      acc += interp(w, wz);
-      if (id1 != cell) {
-        cell = id1;
-        const float4 *p = elem_ptr(q, id1);
-        lo4 = __ldg(p);
-        hi4 = __ldg(p + sys);
-      }
-      w = w1;
-      wz = wz1;
-    }
-    acc = fmaf(rs.last, interp(w, wz), acc);  // exact last segment
-    store(acc * (float)step);
-    return;
-  }
 #pragma unroll 2
   for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
   acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
   store(acc * (float)step);
 }
 
-template <int VG, int CPS, bool FIXS, int PIPE = 0>
+template <int VG, int CPS, bool FIXS>
 __global__ void __launch_bounds__(128 * VG, CPS)
     cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                    const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                    float *__restrict__ out, unsigned zpitch, unsigned ystride) {
-  fp_rays<VG, FIXS, false, PIPE>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
-                                 nullptr);
+  fp_rays<VG, FIXS, false>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride, nullptr);
 }
 
 // The same march storing into row-band destinations (tk_forward_cone_3d_bands).
@@ -648,18 +534,6 @@ static FpKern pick_kernel(bool mirror, bool fixs, int &vg) {
     if (c8x1) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 1, true> : cone_fp_mirror_kernel<8, 1, false>;
     return vg = 4, fixs ? cone_fp_mirror_kernel<4, 3, true> : cone_fp_mirror_kernel<4, 3, false>;
   }
-  if (ce && !strcmp(ce, "8x2P")) return vg = 8, fixs ? cone_fp_kernel<8, 2, true, 1> : cone_fp_kernel<8, 2, false, 1>;
-  if (ce && !strcmp(ce, "4x4P")) return vg = 4, fixs ? cone_fp_kernel<4, 4, true, 1> : cone_fp_kernel<4, 4, false, 1>;
-  if (ce && !strcmp(ce, "4x3P")) return vg = 4, fixs ? cone_fp_kernel<4, 3, true, 1> : cone_fp_kernel<4, 3, false, 1>;
-  if (ce && !strcmp(ce, "6x2P")) return vg = 6, fixs ? cone_fp_kernel<6, 2, true, 1> : cone_fp_kernel<6, 2, false, 1>;
-  if (ce && !strcmp(ce, "8x1P")) return vg = 8, fixs ? cone_fp_kernel<8, 1, true, 1> : cone_fp_kernel<8, 1, false, 1>;
-  if (ce && !strcmp(ce, "4x3Q")) return vg = 4, fixs ? cone_fp_kernel<4, 3, true, 2> : cone_fp_kernel<4, 3, false, 2>;
-  if (ce && !strcmp(ce, "6x2Q")) return vg = 6, fixs ? cone_fp_kernel<6, 2, true, 2> : cone_fp_kernel<6, 2, false, 2>;
-  if (ce && !strcmp(ce, "8x1Q")) return vg = 8, fixs ? cone_fp_kernel<8, 1, true, 2> : cone_fp_kernel<8, 1, false, 2>;
-  if (ce && !strcmp(ce, "5x2Q")) return vg = 5, fixs ? cone_fp_kernel<5, 2, true, 2> : cone_fp_kernel<5, 2, false, 2>;
-  if (ce && !strcmp(ce, "5x2P")) return vg = 5, fixs ? cone_fp_kernel<5, 2, true, 1> : cone_fp_kernel<5, 2, false, 1>;
-  if (ce && !strcmp(ce, "4x2Q")) return vg = 4, fixs ? cone_fp_kernel<4, 2, true, 2> : cone_fp_kernel<4, 2, false, 2>;
-  if (c6x2) return vg = 6, fixs ? cone_fp_kernel<6, 2, true> : cone_fp_kernel<6, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
   return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
 }
