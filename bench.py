@@ -29,6 +29,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import re
 import math
 import os
 import socket
@@ -231,14 +232,21 @@ def ncu_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the newest committed full ncu
     capture of the cfg4 configuration (profiles/ncu_*.json)."""
     caps = list((ROOT / "profiles").glob("ncu_*.json")) + list((ROOT / "profiles").glob("r*/ncu_*.json"))
-    for p in sorted(caps, key=lambda q: q.name, reverse=True):
+    def tag(q):  # ncu_r02aq_... sorts after ncu_r02k_...: (round, letter count, letters)
+        m = re.match(r"ncu_r(\d+)([a-z]*)_", q.name)
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (-1, 0, q.name)
+
+    for p in sorted(caps, key=tag, reverse=True):
         try:
             d = json.loads(p.read_text())
         except (ValueError, OSError):
             continue
         k = d.get(kernel) or {}
         if "dram_bytes_per_launch" in k and k.get("config") == "cfg4-full":
-            return float(k["dram_bytes_per_launch"]), str(p.relative_to(ROOT))
+            # a capture of a launch over a view subset (the back projector runs 720 views as
+            # two launches) is scaled to the whole call the bench times
+            scale = VIEWS / float(k.get("views", VIEWS))
+            return float(k["dram_bytes_per_launch"]) * scale, str(p.relative_to(ROOT))
     return None, None
 
 

@@ -12,9 +12,10 @@
 // detector rows of ONE column: their rays lie in one vertical plane through the
 // source and share the horizontal track, so x / y cell crossings coincide and
 // only z crossings are per lane; the taps are stored z-fastest so a quarter's
-// cells are contiguous.  CTA = a 16-column x 8-row detector tile
-// of VG consecutive views (rays of neighbouring views near the axis share L1
-// lines); CTA order: column blocks, then view groups, then 8-row bands.
+// cells are contiguous.  CTA = an 8-column x 8-row detector tile
+// (two warps of 4 columns x 8 rows) of each of VG = 8 consecutive views (rays of
+// neighbouring views near the axis share L1 lines), 4 CTAs per SM; CTA order:
+// column blocks, then view groups, then 8-row bands.
 //
 // Cells ("coefficient cells", 16 B): cell (z, y, x) of row y holds the bilinear
 // (x, z) polynomial of its four taps, stored (A, C, B, D) for FFMA2 pairs,
@@ -43,7 +44,6 @@
 // more than the L1 misses it removes (git history: tk_fp.cu before 2026-10-17 16:00).
 #include <algorithm>
 #include <cmath>
-#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -53,6 +53,7 @@
 namespace tk {
 
 constexpr int kFpCols = 16, kFpRows = 8;  // detector tile of one view per 128-thread sub-block
+constexpr int kFpColsDefault = 8;         // default launch: 8-column x 8-row view tiles (64 threads)
 constexpr unsigned kFpFixS = 524032u;     // fixed y stride, 16-byte cells (2047 * 256): z pitch == 255 (mod 256)
 constexpr unsigned kMirS = 262138u;       // fixed y stride, 32-byte pair cells (== 250 mod 256): z pitch == 5 (mod 256)
 
@@ -85,39 +86,6 @@ __global__ void __launch_bounds__(256) fp_cells_kernel(const float *__restrict__
     const float A = v00, B = v01 - v00, C = v10 - v00, D = (v11 - v10) - (v01 - v00);
     cq[(unsigned long long)(y + m) * ystride + (unsigned long long)(x + m) * zpitch + (z + m)] =
         make_float4(A, C, B, D);
-  }
-}
-
-// x-row copy for the dual layout: cell (z, x, y) of row x holds the bilinear (y, z)
-// polynomial (A, C, B, D) of its taps, A = V00, B = V01 - V00, C = V10 - V00,
-// D = (V11 - V10) - (V01 - V00) with V_zy at this x.  Tiles of 8 x-rows x 33 y x 33 z
-// (reads: 8 consecutive x per 32-byte sector; writes z-fastest).
-__global__ void __launch_bounds__(256) fp_cells_x_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
-                                                         float4 *__restrict__ cq, unsigned zpitch,
-                                                         unsigned long long xstride) {
-  __shared__ float tile[8][33][34];  // [x - x0][y - y0][z - z0]
-  constexpr int m = kFpMargin;
-  const int pz = nz + 2 * m, py = ny + 2 * m, px = nx + 2 * m;
-  const int z0 = blockIdx.x * 32 - m, y0 = blockIdx.y * 32 - m, x0 = blockIdx.z * 8 - m;
-  for (int e = threadIdx.x; e < 8 * 33 * 33; e += 256) {
-    const int dx = e & 7, r = e >> 3;
-    const int dy = r % 33, dz = r / 33;
-    const int x = x0 + dx, y = y0 + dy, z = z0 + dz;
-    float val = 0.f;
-    if ((unsigned)x < (unsigned)nx && (unsigned)y < (unsigned)ny && (unsigned)z < (unsigned)nz)
-      val = __ldg(vol + ((long long)z * ny + y) * nx + x);
-    tile[dx][dy][dz] = val;
-  }
-  __syncthreads();
-  const int tz = threadIdx.x & 31;
-  for (int i = threadIdx.x >> 5; i < 8 * 32; i += 8) {
-    const int dx = i >> 5, ty = i & 31;
-    const int z = z0 + tz, y = y0 + ty, x = x0 + dx;  // cell (z, x, y) of the padded grid
-    if (z + m >= pz || y + m >= py || x + m >= px) continue;
-    const float v00 = tile[dx][ty][tz], v01 = tile[dx][ty + 1][tz], v10 = tile[dx][ty][tz + 1],
-                v11 = tile[dx][ty + 1][tz + 1];
-    const float A = v00, B = v01 - v00, C = v10 - v00, D = (v11 - v10) - (v01 - v00);
-    cq[(unsigned long long)(x + m) * xstride + (unsigned long long)(y + m) * zpitch + (z + m)] = make_float4(A, C, B, D);
   }
 }
 
@@ -200,28 +168,18 @@ struct FpDests {
   long long view_stride;
 };
 
-__device__ __forceinline__ int nfull_of(const RaySetup &rs) { return rs.n - 1; }
-
-template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int ORDER = 0, bool DUAL = false,
-          bool DUAL_CARRY = true>
-__device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, const float4 *__restrict__ qx, int nx, int ny, int nz, double sx, double sy,
+template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols>
+__device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
                                         unsigned ystride, const FpDests *dests) {
-  constexpr int SUB = COLS * kFpRows;  // threads per view sub-block
+  constexpr int SUB = COLS * kFpRows;  // threads per view: COLS columns x 8 rows (warps of 4 x 8)
   const int ncb = (cols + COLS - 1) / COLS;
   const unsigned b = blockIdx.x;
+  const int cb = (int)(b % ncb);
+  const unsigned bt = b / ncb;
   const int nvg = (n_views + VG - 1) / VG;
-  int cb, v0, rb;
-  if (ORDER == 0) {  // column blocks, then view groups, then row bands
-    cb = (int)(b % ncb);
-    const unsigned bt = b / ncb;
-    v0 = (int)(bt % nvg) * VG, rb = (int)(bt / nvg);
-  } else {  // view groups, then column blocks, then row bands
-    v0 = (int)(b % nvg) * VG;
-    const unsigned bt = b / nvg;
-    cb = (int)(bt % ncb), rb = (int)(bt / ncb);
-  }
+  const int v0 = (int)(bt % nvg) * VG, rb = (int)(bt / nvg);
   const int sub = threadIdx.x / SUB, t = threadIdx.x % SUB;
   const int v = v0 + sub, c = cb * COLS + (t >> 3), r = rb * kFpRows + (t & 7);
   if (c >= cols || r >= rows || v >= n_views) return;
@@ -245,72 +203,8 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, const floa
   const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
   const float magic = 8388608.f;  // coordinates >= 0: floor(f) = bits(f + 2^23) - 0x4B000000
   const unsigned sys = FIXS ? kFpFixS : ystride;
-  const float gz = rs.gz;
-  if (DUAL) {
-    // Row axis = the ray's major horizontal axis: the y-row copy q (cells (z, y, x) of row
-    // y, bilinear in (x, z)) or the x-row copy qx (cells (z, x, y) of row x, bilinear in
-    // (y, z)); most cell changes are then row steps, where the far row the ray moves into
-    // is the only new one: the near row is carried over in registers (one LDG.128).
-    const bool xrow = fabsf(rs.gx) > fabsf(rs.gy);
-    // one base pointer: the x-row copy follows the y-row copy, at a per-ray cell offset
-    const unsigned off = xrow ? (unsigned)(qx - q) : 0u;
-    const float ea = xrow ? ey : ex, eb = xrow ? ex : ey, ga = xrow ? rs.gy : rs.gx, gb = xrow ? rs.gx : rs.gy;
-    const unsigned long long e2 = pk2(ea, eb), g2 = pk2(ga, gb), m2 = pk2(magic, magic);
-    auto cell_of = [&](float kk, unsigned long long &fab, unsigned long long &xab, float &fz, float &xz) {
-      fab = ffma2(pk2(kk, kk), g2, e2);
-      fz = fmaf(kk, gz, ez);
-      xab = fadd2_rm(fab, m2);
-      xz = __fadd_rd(fz, magic);
-      const float2 xb = upk2(xab);
-      return __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + (__float_as_uint(xz) + off));
-    };
-    float4 lo4, hi4;
-    unsigned cell;
-    {
-      unsigned long long fab, xab;
-      float fz, xz;
-      cell = cell_of(nfull_of(rs) > 0 ? 0.5f : 0.5f * rs.last, fab, xab, fz, xz);
-      const float4 *p = elem_ptr(q, cell);
-      lo4 = __ldg(p);
-      hi4 = __ldg(p + sys);
-    }
-    // CARRY: lead = the row the ray moves into (b + 1 going up, b going down), trail = the
-    // other; a row step makes the lead row the trail row and loads only the new lead row
-    auto march = [&](auto up_tag) -> float {
-      constexpr bool UP = decltype(up_tag)::value;
-      float4 &lead = UP ? hi4 : lo4, &trail = UP ? lo4 : hi4;
-      const unsigned lead_off = UP ? sys : 0u, trail_off = UP ? 0u : sys;
-      auto sample = [&](float kk) -> float {
-        unsigned long long fab, xab;
-        float fz, xz;
-        const unsigned id = cell_of(kk, fab, xab, fz, xz);
-        if (id != cell) {
-          if (DUAL_CARRY && id == (UP ? cell + sys : cell - sys)) {
-            trail = lead;
-          } else {
-            trail = __ldg(elem_ptr(q, id + trail_off));
-          }
-          lead = __ldg(elem_ptr(q, id + lead_off));
-          cell = id;
-        }
-        const float2 w = upk2(fsub2(fab, fsub2(xab, m2)));
-        const float wz = fz - (xz - magic);
-        const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
-        const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
-        const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
-        return lerpf(s0, s1, w.y);
-      };
-      float acc = 0.f, kf = 0.5f;
-      const int nfull = rs.n - 1;
-#pragma unroll 2
-      for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
-      return fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
-    };
-    const float acc = gb > 0.f ? march(std::true_type{}) : march(std::false_type{});
-    store(acc * (float)step);
-    return;
-  }
   const unsigned long long e2 = pk2(ex, ey), g2 = pk2(rs.gx, rs.gy), m2 = pk2(magic, magic);
+  const float gz = rs.gz;
   unsigned cell = 0xffffffffu;
   float4 lo4 = make_float4(0.f, 0.f, 0.f, 0.f), hi4 = lo4;
   auto sample = [&](float kk) -> float {
@@ -342,30 +236,29 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, const floa
   store(acc * (float)step);
 }
 
-template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int ORDER = 0, bool DUAL = false, bool DUAL_CARRY = true>
+template <int VG, int CPS, bool FIXS, int COLS = kFpCols>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
-    cone_fp_kernel(const float4 *__restrict__ q, const float4 *__restrict__ qx, int nx, int ny, int nz, double sx,
-                   double sy, double sz, const ConeRayView *__restrict__ views, int rows, int cols, int n_views,
-                   double step, float *__restrict__ out, unsigned zpitch, unsigned ystride) {
-  fp_rays<VG, FIXS, false, COLS, ORDER, DUAL, DUAL_CARRY>(q, qx, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out,
-                                              zpitch, ystride, nullptr);
+    cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
+                   const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
+                   float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+  fp_rays<VG, FIXS, false, COLS>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
+                                 nullptr);
 }
 
 // The same march storing into row-band destinations (tk_forward_cone_3d_bands).
 template <bool FIXS>
-__global__ void __launch_bounds__(1024, 2)
+__global__ void __launch_bounds__(kFpColsDefault * kFpRows * 8, 4)
     cone_fp_bands_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                          const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                          unsigned zpitch, unsigned ystride, const __grid_constant__ FpDests dests) {
-  fp_rays<8, FIXS, true>(q, nullptr, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, nullptr, zpitch, ystride,
-                         &dests);
+  fp_rays<8, FIXS, true, kFpColsDefault>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, nullptr, zpitch,
+                                         ystride, &dests);
 }
 
 // Sub-block = 16 columns x 8 direct rows (lower detector half) plus their 8 mirror rows.
 template <int VG, int CPS, bool FIXS>
 __global__ void __launch_bounds__(128 * VG, CPS)
-    cone_fp_mirror_kernel(const float4 *__restrict__ q, const float4 *__restrict__ /*qx: unused*/, int nx, int ny,
-                          int nz, double sx, double sy, double sz,
+    cone_fp_mirror_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                           const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                           float *__restrict__ out, unsigned zpitch, unsigned ystride) {
   const int half = (rows + 1) >> 1;  // direct rows [0, half); an odd detector's middle row is its own mirror
@@ -518,7 +411,7 @@ bool views_z_mirror(const double *sources, const double *minv, int n_views, int 
 // load offset) when it fits and its padding is affordable (make_layout);
 // otherwise a runtime stride with bias-free pitches: zp (1 + xp) == -1 (mod 256).
 struct FpLayout {
-  bool mirror = false, fixs = false, dual = false;  // dual: y-row copy then x-row copy, same strides
+  bool mirror = false, fixs = false;
   unsigned zpitch = 0, xpitch = 0, ystride = 0;
   int zcells = 0;  // padded z cells stored per (y, x)
   size_t cell_bytes = 16;
@@ -529,19 +422,15 @@ static int env_int(const char *name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
-static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L, bool force_runtime_stride = false,
-                        bool dual = false) {
+static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L, bool force_runtime_stride = false) {
   constexpr int m2 = 2 * kFpMargin;
   L = FpLayout();
   L.mirror = mirror;
-  L.dual = dual && !mirror;
   L.cell_bytes = mirror ? 32 : 16;
   // direct rays of the mirror kernel reach padded z <= K / 2 (+ rounding); taps floor, floor + 1
   L.zcells = mirror ? (nz - 1 + m2) / 2 + 2 : nz + m2;
-  // dual: the x-row copy's columns are y, so the row pitch covers max(nx, ny)
-  const unsigned zc = (unsigned)L.zcells, xc = (unsigned)((L.dual ? std::max(nx, ny) : nx) + m2);
-  const unsigned long long rows = L.dual ? (unsigned long long)(std::max(nx, ny) + m2)
-                                         : (unsigned long long)(ny + m2);  // rows per copy
+  const unsigned zc = (unsigned)L.zcells, xc = (unsigned)(nx + m2);
+  const unsigned long long rows = (unsigned long long)(ny + m2);
   const unsigned long long compact = rows * xc * zc;
   const unsigned fixs = mirror ? kMirS : kFpFixS, zres = mirror ? 5u : 255u;
   const unsigned zpf = zc + (zres + 256u - zc % 256u) % 256u;
@@ -549,9 +438,8 @@ static bool make_layout(int nz, int ny, int nx, bool mirror, FpLayout &L, bool f
   // the fixed stride pads each row to kFpFixS cells: allowed while that costs at most 2x the
   // compact layout or at most 3 GB (cfg3 256^3: 2.2 GB, 9 % faster); an allocation failure
   // falls back to the compact layout (plan_cells)
-  const unsigned long long ncopy = L.dual ? 2 : 1;
-  const unsigned long long fixed_bytes = ncopy * rows * fixs * L.cell_bytes;
-  const bool affordable = rows * fixs <= 2 * compact || fixed_bytes <= (ncopy * 3ull << 30);
+  const unsigned long long fixed_bytes = rows * fixs * L.cell_bytes;
+  const bool affordable = rows * fixs <= 2 * compact || fixed_bytes <= (3ull << 30);
   if (!nofix && (unsigned long long)xc * zpf <= fixs && affordable && rows * fixs < (1ull << 32)) {
     L.fixs = true;
     L.zpitch = zpf;
@@ -591,30 +479,22 @@ struct FpPlan {
   const float *vol = nullptr;
   int nz = 0, ny = 0, nx = 0;
   double sz = 0, sy = 0, sx = 0;
-  FpLayout lay[3];             // [general, mirror, dual]
-  void *cells[3] = {nullptr, nullptr, nullptr};
+  FpLayout lay[2];             // [general, mirror]
+  void *cells[2] = {nullptr, nullptr};
 };
 
-enum { kFpGeneral = 0, kFpMirrorKind = 1, kFpDual = 2 };
-
-// cells of the dual layout's x-row copy (after the y-row copy's rows)
-static const float4 *x_copy(const FpPlan &pl) {
-  return static_cast<const float4 *>(pl.cells[kFpDual]) + (size_t)(pl.ny + 2 * kFpMargin) * pl.lay[kFpDual].ystride;
-}
-
-static int plan_cells(FpPlan &pl, int k, cudaStream_t st) {
+static int plan_cells(FpPlan &pl, bool mirror, cudaStream_t st) {
+  const int k = mirror ? 1 : 0;
   if (pl.cells[k]) return TK_OK;
   FpLayout &L = pl.lay[k];
-  const bool mirror = k == kFpMirrorKind, dual = k == kFpDual;
-  if (!make_layout(pl.nz, pl.ny, pl.nx, mirror, L, false, dual))
+  if (!make_layout(pl.nz, pl.ny, pl.nx, mirror, L))
     return fail_arg("tk_forward_cone_3d: volume too large for 32-bit cell indices");
-  const size_t rows = (size_t)(pl.ny + 2 * kFpMargin) + (dual ? (size_t)(pl.nx + 2 * kFpMargin) : 0);
-  size_t bytes = L.cell_bytes * rows * L.ystride;
+  size_t bytes = L.cell_bytes * (size_t)(pl.ny + 2 * kFpMargin) * L.ystride;
   cudaError_t e = cudaMallocAsync(&pl.cells[k], bytes, st);
   if (e == cudaErrorMemoryAllocation && L.fixs) {  // the fixed stride pads: retry with the compact layout
     (void)cudaGetLastError();
-    make_layout(pl.nz, pl.ny, pl.nx, mirror, L, true, dual);
-    bytes = L.cell_bytes * rows * L.ystride;
+    make_layout(pl.nz, pl.ny, pl.nx, mirror, L, true);
+    bytes = L.cell_bytes * (size_t)(pl.ny + 2 * kFpMargin) * L.ystride;
     e = cudaMallocAsync(&pl.cells[k], bytes, st);
   }
   if (e != cudaSuccess) {
@@ -631,13 +511,6 @@ static int plan_cells(FpPlan &pl, int k, cudaStream_t st) {
     fp_cells_kernel<<<g, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, static_cast<float4 *>(pl.cells[k]), L.zpitch,
                                        L.ystride);
     TK_LAUNCHED("fp_cells_kernel");
-    if (dual) {
-      dim3 gx(ceil_div(pl.nz + 2 * kFpMargin, 32), ceil_div(pl.ny + 2 * kFpMargin, 32),
-              ceil_div(pl.nx + 2 * kFpMargin, 8));
-      fp_cells_x_kernel<<<gx, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, const_cast<float4 *>(x_copy(pl)), L.zpitch,
-                                            L.ystride);
-      TK_LAUNCHED("fp_cells_x_kernel");
-    }
   }
   return TK_OK;
 }
@@ -650,47 +523,36 @@ static void plan_free(FpPlan &pl, cudaStream_t st) {
     }
 }
 
-using FpKern = void (*)(const float4 *, const float4 *, int, int, int, double, double, double, const ConeRayView *, int, int, int,
+using FpKern = void (*)(const float4 *, int, int, int, double, double, double, const ConeRayView *, int, int, int,
                         double, float *, unsigned, unsigned);
 
-// Launch configurations (views per CTA x CTAs per SM): general 8x2 (default:
-// 32 registers, 64 warps/SM) or 4x4; mirror 4x3 (default, 40 registers), 8x2, 8x1.
-static FpKern pick_kernel(bool mirror, bool fixs, bool dual, int &vg, int &tcols) {
+// Launch configurations (views per CTA x CTAs per SM): general 8x4 with 8-column view
+// tiles (default: 32 registers, 64 warps/SM; 420.6 vs 423.7 ms for 16-column tiles at
+// 8x2, profiles/r02/fp_ab_r02ap.log), 8x2 or 4x4 with 16-column tiles; mirror 4x3
+// (default, 40 registers), 8x2, 8x1.
+static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
   tcols = kFpCols;
   const char *ce = getenv("TK_FP_CFG");
   const bool c8x1 = ce && !strcmp(ce, "8x1"), c8x2 = ce && !strcmp(ce, "8x2"), c4x4 = ce && !strcmp(ce, "4x4"),
-             c4x3 = ce && !strcmp(ce, "4x3"), c6x2 = ce && !strcmp(ce, "6x2"), c8x4c8 = ce && !strcmp(ce, "8x4c8");
+             c4x3 = ce && !strcmp(ce, "4x3"), c6x2 = ce && !strcmp(ce, "6x2");
   if (mirror) {
     if (c6x2) return vg = 6, fixs ? cone_fp_mirror_kernel<6, 2, true> : cone_fp_mirror_kernel<6, 2, false>;
     if (c8x2) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 2, true> : cone_fp_mirror_kernel<8, 2, false>;
     if (c8x1) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 1, true> : cone_fp_mirror_kernel<8, 1, false>;
     return vg = 4, fixs ? cone_fp_mirror_kernel<4, 3, true> : cone_fp_mirror_kernel<4, 3, false>;
   }
-  if (dual && env_int("TK_FP_DUAL", 0) == 2) {  // dual layout without the row carry-over
-    if (c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 3, true, 16, 0, true, false> : cone_fp_kernel<4, 3, false, 16, 0, true, false>;
-    return vg = 8, fixs ? cone_fp_kernel<8, 2, true, 16, 0, true, false> : cone_fp_kernel<8, 2, false, 16, 0, true, false>;
-  }
-  if (dual) {
-    if (c8x4c8)
-      return vg = 8, tcols = 8,
-             fixs ? cone_fp_kernel<8, 4, true, 8, 0, true> : cone_fp_kernel<8, 4, false, 8, 0, true>;
-    if (c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 3, true, 16, 0, true> : cone_fp_kernel<4, 3, false, 16, 0, true>;
-    if (c6x2) return vg = 6, fixs ? cone_fp_kernel<6, 2, true, 16, 0, true> : cone_fp_kernel<6, 2, false, 16, 0, true>;
-    return vg = 8, fixs ? cone_fp_kernel<8, 2, true, 16, 0, true> : cone_fp_kernel<8, 2, false, 16, 0, true>;
-  }
-  if (c8x4c8) return vg = 8, tcols = 8, fixs ? cone_fp_kernel<8, 4, true, 8> : cone_fp_kernel<8, 4, false, 8>;
+  if (c8x2) return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
-  return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
+  return vg = 8, tcols = kFpColsDefault,
+         fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault> : cone_fp_kernel<8, 4, false, kFpColsDefault>;
 }
 
 static int plan_project(FpPlan &pl, const double *sources, const double *minv, int n_views, int rows, int cols,
                         double step, float *out, cudaStream_t st) {
   const bool mirror = fp_use_mirror(sources, minv, n_views, rows, pl.nz, pl.ny, pl.nx);
-  const bool dual = !mirror && env_int("TK_FP_DUAL", 0) != 0;
-  const int kind = mirror ? kFpMirrorKind : dual ? kFpDual : kFpGeneral;
-  int rc = plan_cells(pl, kind, st);
+  int rc = plan_cells(pl, mirror, st);
   if (rc != TK_OK) return rc;
-  const FpLayout &L = pl.lay[kind];
+  const FpLayout &L = pl.lay[mirror ? 1 : 0];
   std::vector<ConeRayView> hv(n_views);
   for (int i = 0; i < n_views; ++i) {
     for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
@@ -698,25 +560,25 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
   }
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
-  const float4 *cells = static_cast<const float4 *>(pl.cells[kind]);
   const char *algo = getenv("TK_FP_ALGO");
   if (!mirror && algo && !strcmp(algo, "warp")) {  // warp-cooperative comparison kernel
     const long long nbw = (long long)ceil_div(cols, kFpCols) * ceil_div(rows, kFpRows) * n_views;
     if (nbw >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kw = L.fixs ? cone_fp_warp_kernel<true> : cone_fp_warp_kernel<false>;
-    kw<<<(unsigned)nbw, 128, 0, st>>>(cells, pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<ConeRayView>(), rows,
-                                      cols, n_views, step, out, L.zpitch, L.ystride);
+    kw<<<(unsigned)nbw, 128, 0, st>>>(static_cast<const float4 *>(pl.cells[0]), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy,
+                                      pl.sz, dviews.as<ConeRayView>(), rows, cols, n_views, step, out, L.zpitch,
+                                      L.ystride);
     TK_LAUNCHED("cone_fp_warp_kernel");
     return TK_OK;
   }
   int vg = 1, tcols = kFpCols;
-  FpKern kern = pick_kernel(mirror, L.fixs, dual, vg, tcols);
+  FpKern kern = pick_kernel(mirror, L.fixs, vg, tcols);
   const int brows = mirror ? (rows + 1) / 2 : rows;
   const long long nb = (long long)ceil_div(cols, tcols) * ceil_div(brows, kFpRows) * ceil_div(n_views, vg);
   if (nb >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-  kern<<<(unsigned)nb, tcols * kFpRows * vg, 0, st>>>(cells, dual ? x_copy(pl) : nullptr, pl.nx, pl.ny, pl.nz, pl.sx,
-                                                      pl.sy, pl.sz, dviews.as<ConeRayView>(), rows, cols, n_views,
-                                                      step, out, L.zpitch, L.ystride);
+  kern<<<(unsigned)nb, tcols * kFpRows * vg, 0, st>>>(static_cast<const float4 *>(pl.cells[mirror ? 1 : 0]), pl.nx, pl.ny, pl.nz,
+                                          pl.sx, pl.sy, pl.sz, dviews.as<ConeRayView>(), rows, cols, n_views, step, out,
+                                          L.zpitch, L.ystride);
   TK_LAUNCHED(mirror ? "cone_fp_mirror_kernel" : "cone_fp_kernel");
   return TK_OK;
 }
@@ -724,9 +586,9 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
 // Fused view-sharded projection + row-band exchange: the general kernel with BANDS stores.
 static int plan_project_bands(FpPlan &pl, const double *sources, const double *minv, int n_views, int rows, int cols,
                               double step, const FpDests &d, cudaStream_t st) {
-  int rc = plan_cells(pl, kFpGeneral, st);
+  int rc = plan_cells(pl, false, st);
   if (rc != TK_OK) return rc;
-  const FpLayout &L = pl.lay[kFpGeneral];
+  const FpLayout &L = pl.lay[0];
   std::vector<ConeRayView> hv(n_views);
   for (int i = 0; i < n_views; ++i) {
     for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
@@ -734,10 +596,10 @@ static int plan_project_bands(FpPlan &pl, const double *sources, const double *m
   }
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
-  const long long nb = (long long)ceil_div(cols, kFpCols) * ceil_div(rows, kFpRows) * ceil_div(n_views, 8);
+  const long long nb = (long long)ceil_div(cols, kFpColsDefault) * ceil_div(rows, kFpRows) * ceil_div(n_views, 8);
   if (nb >= (1LL << 31)) return fail_arg("tk_forward_cone_3d_bands: problem too large for one launch");
   auto kern = L.fixs ? cone_fp_bands_kernel<true> : cone_fp_bands_kernel<false>;
-  kern<<<(unsigned)nb, 1024, 0, st>>>(static_cast<const float4 *>(pl.cells[0]), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
+  kern<<<(unsigned)nb, kFpColsDefault * kFpRows * 8, 0, st>>>(static_cast<const float4 *>(pl.cells[0]), pl.nx, pl.ny, pl.nz, pl.sx, pl.sy, pl.sz,
                                       dviews.as<ConeRayView>(), rows, cols, n_views, step, L.zpitch, L.ystride, d);
   TK_LAUNCHED("cone_fp_bands_kernel");
   return TK_OK;
