@@ -168,7 +168,10 @@ struct FpDests {
   long long view_stride;
 };
 
-template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols>
+// PROBE (roofline decomposition, TK_FP_PROBE; not a projector): 1 = the march with its
+// cell loads but a 1-FADD "interpolation" (the access stream alone), 2 = the full
+// arithmetic on cell values synthesised from the cell index instead of loaded.
+template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
@@ -216,10 +219,17 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
     const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
     if (id != cell) {
       cell = id;
-      const float4 *p = elem_ptr(q, id);
-      lo4 = __ldg(p);
-      hi4 = __ldg(p + sys);
+      if (PROBE == 2) {
+        lo4.x = __uint_as_float((id & 0x7fffu) | 0x3f800000u);
+        lo4 = make_float4(lo4.x, lo4.x, lo4.x, lo4.x);
+        hi4 = lo4;
+      } else {
+        const float4 *p = elem_ptr(q, id);
+        lo4 = __ldg(p);
+        hi4 = __ldg(p + sys);
+      }
     }
+    if (PROBE == 1) return lo4.x + hi4.w;
     const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
     const float wz = fz - (xz - magic);
     const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
@@ -230,18 +240,56 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   float acc = 0.f;
   float kf = 0.5f;
   const int nfull = rs.n - 1;
+  if (PROBE == 3) {
+    // z axis of two consecutive samples as one FFMA2 / FADD2.RM / 2 FADD2 (the x / y pair of
+    // each sample is already packed): the same values as sample(), bit for bit
+    auto sample_xy = [&](float kk, float xz, float wz) -> float {
+      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
+      const unsigned long long xxy = fadd2_rm(fxy, m2);
+      const float2 xb = upk2(xxy);
+      const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
+      if (id != cell) {
+        cell = id;
+        const float4 *p = elem_ptr(q, id);
+        lo4 = __ldg(p);
+        hi4 = __ldg(p + sys);
+      }
+      const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
+      const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
+      const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
+      const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
+      return lerpf(s0, s1, w.y);
+    };
+    unsigned long long kk2 = pk2(0.5f, 1.5f);
+    const unsigned long long two2 = pk2(2.f, 2.f), gz2 = pk2(gz, gz), ez2 = pk2(ez, ez);
+    int k = 0;
+#pragma unroll 1
+    for (; k + 1 < nfull; k += 2) {
+      const unsigned long long fz2 = ffma2(kk2, gz2, ez2);
+      const unsigned long long xz2 = fadd2_rm(fz2, m2);
+      const float2 wz = upk2(fsub2(fz2, fsub2(xz2, m2)));
+      const float2 xz = upk2(xz2), kk = upk2(kk2);
+      acc += sample_xy(kk.x, xz.x, wz.x);
+      acc += sample_xy(kk.y, xz.y, wz.y);
+      kk2 = fadd2(kk2, two2);
+    }
+    if (k < nfull) acc += sample((float)k + 0.5f);
+    acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
+    store(acc * (float)step);
+    return;
+  }
 #pragma unroll 2
   for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
   acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
   store(acc * (float)step);
 }
 
-template <int VG, int CPS, bool FIXS, int COLS = kFpCols>
+template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                    const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                    float *__restrict__ out, unsigned zpitch, unsigned ystride) {
-  fp_rays<VG, FIXS, false, COLS>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
+  fp_rays<VG, FIXS, false, COLS, PROBE>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
                                  nullptr);
 }
 
@@ -541,6 +589,16 @@ static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
     if (c8x1) return vg = 8, fixs ? cone_fp_mirror_kernel<8, 1, true> : cone_fp_mirror_kernel<8, 1, false>;
     return vg = 4, fixs ? cone_fp_mirror_kernel<4, 3, true> : cone_fp_mirror_kernel<4, 3, false>;
   }
+  const int probe = env_int("TK_FP_PROBE", 0);  // roofline decomposition probes (not projectors)
+  if (probe == 1)
+    return vg = 8, tcols = kFpColsDefault,
+           fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 1> : cone_fp_kernel<8, 4, false, kFpColsDefault, 1>;
+  if (probe == 2)
+    return vg = 8, tcols = kFpColsDefault,
+           fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 2> : cone_fp_kernel<8, 4, false, kFpColsDefault, 2>;
+  if (probe == 3)
+    return vg = 8, tcols = kFpColsDefault,
+           fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 3> : cone_fp_kernel<8, 4, false, kFpColsDefault, 3>;
   if (c8x2) return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
   return vg = 8, tcols = kFpColsDefault,
