@@ -240,44 +240,6 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   float acc = 0.f;
   float kf = 0.5f;
   const int nfull = rs.n - 1;
-  if (PROBE == 3) {
-    // z axis of two consecutive samples as one FFMA2 / FADD2.RM / 2 FADD2 (the x / y pair of
-    // each sample is already packed): the same values as sample(), bit for bit
-    auto sample_xy = [&](float kk, float xz, float wz) -> float {
-      const unsigned long long fxy = ffma2(pk2(kk, kk), g2, e2);
-      const unsigned long long xxy = fadd2_rm(fxy, m2);
-      const float2 xb = upk2(xxy);
-      const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
-      if (id != cell) {
-        cell = id;
-        const float4 *p = elem_ptr(q, id);
-        lo4 = __ldg(p);
-        hi4 = __ldg(p + sys);
-      }
-      const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
-      const float2 tl = upk2(ffma2(pk2(lo4.z, lo4.w), pk2(w.x, w.x), pk2(lo4.x, lo4.y)));
-      const float2 th = upk2(ffma2(pk2(hi4.z, hi4.w), pk2(w.x, w.x), pk2(hi4.x, hi4.y)));
-      const float s0 = fmaf(wz, tl.y, tl.x), s1 = fmaf(wz, th.y, th.x);
-      return lerpf(s0, s1, w.y);
-    };
-    unsigned long long kk2 = pk2(0.5f, 1.5f);
-    const unsigned long long two2 = pk2(2.f, 2.f), gz2 = pk2(gz, gz), ez2 = pk2(ez, ez);
-    int k = 0;
-#pragma unroll 1
-    for (; k + 1 < nfull; k += 2) {
-      const unsigned long long fz2 = ffma2(kk2, gz2, ez2);
-      const unsigned long long xz2 = fadd2_rm(fz2, m2);
-      const float2 wz = upk2(fsub2(fz2, fsub2(xz2, m2)));
-      const float2 xz = upk2(xz2), kk = upk2(kk2);
-      acc += sample_xy(kk.x, xz.x, wz.x);
-      acc += sample_xy(kk.y, xz.y, wz.y);
-      kk2 = fadd2(kk2, two2);
-    }
-    if (k < nfull) acc += sample((float)k + 0.5f);
-    acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
-    store(acc * (float)step);
-    return;
-  }
 #pragma unroll 2
   for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
   acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
@@ -596,9 +558,6 @@ static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
   if (probe == 2)
     return vg = 8, tcols = kFpColsDefault,
            fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 2> : cone_fp_kernel<8, 4, false, kFpColsDefault, 2>;
-  if (probe == 3)
-    return vg = 8, tcols = kFpColsDefault,
-           fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 3> : cone_fp_kernel<8, 4, false, kFpColsDefault, 3>;
   if (c8x2) return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
   return vg = 8, tcols = kFpColsDefault,
