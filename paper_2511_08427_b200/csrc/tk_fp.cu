@@ -266,20 +266,21 @@ __global__ void __launch_bounds__(kFpColsDefault * kFpRows * 8, 4)
 }
 
 // Sub-block = 16 columns x 8 direct rows (lower detector half) plus their 8 mirror rows.
-template <int VG, int CPS, bool FIXS>
-__global__ void __launch_bounds__(128 * VG, CPS)
+template <int VG, int CPS, bool FIXS, int COLS = kFpCols>
+__global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_mirror_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                           const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                           float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+  constexpr int SUB = COLS * kFpRows;
   const int half = (rows + 1) >> 1;  // direct rows [0, half); an odd detector's middle row is its own mirror
-  const int ncb = (cols + kFpCols - 1) / kFpCols;
+  const int ncb = (cols + COLS - 1) / COLS;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
   const unsigned bt = b / ncb;
   const int nvg = (n_views + VG - 1) / VG;
   const int v0 = (int)(bt % nvg) * VG, rb = (int)(bt / nvg);
-  const int sub = threadIdx.x >> 7, t = threadIdx.x & 127;
-  const int v = v0 + sub, c = cb * kFpCols + (t >> 3), r = rb * kFpRows + (t & 7);
+  const int sub = threadIdx.x / SUB, t = threadIdx.x % SUB;
+  const int v = v0 + sub, c = cb * COLS + (t >> 3), r = rb * kFpRows + (t & 7);
   if (c >= cols || r >= half || v >= n_views) return;
   const int rm = rows - 1 - r;
   float *dst = out + ((long long)v * rows + r) * cols + c;
