@@ -119,27 +119,6 @@ int tk_fp_plan_project(void *plan, const double *sources, const double *minv,
                        int n_views, int rows, int cols, double step, float *out,
                        void *stream);
 int tk_fp_plan_destroy(void *plan, void *stream);
-/* Upload-ordered forward projection (no reference counterpart; ops.py_forward_project's
- * pipeline): the volume arrives in z slabs, the cells of each arrived part are built, and
- * detector row bands are projected as soon as every volume row their rays can touch is
- * in.  tk_fp_plan_cells: volume rows [z0, z1) of `vol` are present (one contiguous
- * range that only grows between calls); builds every cell computable from them.
- * tk_fp_plan_project_rows: as tk_fp_plan_project for detector rows [row0, row1) only
- * (whole 8-row bands; out is the full (n_views, rows, cols) sinogram), from the cells
- * built so far (all of them when tk_fp_plan_cells was never called).
- * tk_fp_band_z: for each 8-row band b, zlo[b]..zhi[b] = the volume z rows the taps of
- * its samples can touch over all views and columns (zlo > zhi: no ray hits the
- * volume); host outputs, synchronises `stream`.
- * tk_copy_2d: cudaMemcpy2DAsync (any direction) -- row-band copies of a sinogram. */
-int tk_fp_plan_cells(void *plan, int z0, int z1, void *stream);
-int tk_fp_plan_project_rows(void *plan, const double *sources, const double *minv,
-                            int n_views, int rows, int cols, int row0, int row1,
-                            double step, float *out, void *stream);
-int tk_fp_band_z(const double *sources, const double *minv, int n_views, int rows, int cols,
-                 int nz, int ny, int nx, double sz, double sy, double sx, double step,
-                 int *zlo, int *zhi, void *stream);
-int tk_copy_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width,
-               size_t height, void *stream);
 /* replaces _kernels.back_cone_3d (_kernels.py:281-322) as called from
  * projectors.back_project_cone_3d (projectors.py:228-248).
  * sino (V,rows,cols) device; mats host float64 (V,3,4); out (nz,ny,nx). */

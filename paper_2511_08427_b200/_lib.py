@@ -50,11 +50,6 @@ SIGNATURES = {
                           ctypes.POINTER(ctypes.c_void_p), _ptr],
     "tk_fp_plan_project": [_ptr, _dptr, _dptr, _c_int, _c_int, _c_int, _c_dbl, _ptr, _ptr],
     "tk_fp_plan_destroy": [_ptr, _ptr],
-    "tk_fp_plan_cells": [_ptr, _c_int, _c_int, _ptr],
-    "tk_fp_plan_project_rows": [_ptr, _dptr, _dptr, _c_int, _c_int, _c_int, _c_int, _c_int, _c_dbl, _ptr, _ptr],
-    "tk_fp_band_z": [_dptr, _dptr, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl,
-                     _c_dbl, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), _ptr],
-    "tk_copy_2d": [_ptr, ctypes.c_size_t, _ptr, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, _ptr],
     "tk_back_cone_3d": [_ptr, _c_int, _c_int, _c_int, _dptr, _c_dbl, _c_int, _c_int, _c_int, _c_int,
                         _c_dbl, _c_dbl, _c_dbl, _ptr, _ptr],
     "tk_back_cone_3d_ex": [_ptr, _c_int, _c_int, _c_int, _c_int, _c_int, _dptr, _c_dbl, _c_int,

@@ -43,7 +43,6 @@
 // extrapolated to infinitely thick slabs -- the per-slab CTA-wide lockstep costs
 // more than the L1 misses it removes (git history: tk_fp.cu before 2026-10-17 16:00).
 #include <algorithm>
-#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -62,15 +61,13 @@ constexpr unsigned kMirS = 262138u;       // fixed y stride, 32-byte pair cells 
 // layouts
 // ---------------------------------------------------------------------------
 // 32 (z) x 32 (x) tiles of one y row: reads along x, writes along z (coalesced).
-// Cells of padded z in [zc0, zc1) only (tiles from zc0): the volume rows those cells
-// read (zc0 - m .. zc1 - m) may be all that has arrived (tk_fp_plan_cells).
 __global__ void __launch_bounds__(256) fp_cells_kernel(const float *__restrict__ vol, int nz, int ny, int nx,
                                                        float4 *__restrict__ cq, unsigned zpitch,
-                                                       unsigned long long ystride, int zc0, int zc1) {
+                                                       unsigned long long ystride) {
   __shared__ float tile[33][34];  // [x - x0][z - z0]
   constexpr int m = kFpMargin;
-  const int pz = min(nz + 2 * m, zc1), px = nx + 2 * m;
-  const int z0 = zc0 + blockIdx.x * 32 - m, x0 = blockIdx.y * 32 - m, y = (int)blockIdx.z - m;
+  const int pz = nz + 2 * m, px = nx + 2 * m;
+  const int z0 = blockIdx.x * 32 - m, x0 = blockIdx.y * 32 - m, y = (int)blockIdx.z - m;
   const bool yin = (unsigned)y < (unsigned)ny;
   for (int e = threadIdx.x; e < 33 * 33; e += 256) {
     const int dx = e % 33, dz = e / 33;
@@ -178,14 +175,14 @@ template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
-                                        unsigned ystride, const FpDests *dests, int rb0 = 0) {
+                                        unsigned ystride, const FpDests *dests) {
   constexpr int SUB = COLS * kFpRows;  // threads per view: COLS columns x 8 rows (warps of 4 x 8)
   const int ncb = (cols + COLS - 1) / COLS;
   const unsigned b = blockIdx.x;
   const int cb = (int)(b % ncb);
   const unsigned bt = b / ncb;
   const int nvg = (n_views + VG - 1) / VG;
-  const int v0 = (int)(bt % nvg) * VG, rb = rb0 + (int)(bt / nvg);  // rb0: first 8-row band of the launch
+  const int v0 = (int)(bt % nvg) * VG, rb = (int)(bt / nvg);
   const int sub = threadIdx.x / SUB, t = threadIdx.x % SUB;
   const int v = v0 + sub, c = cb * COLS + (t >> 3), r = rb * kFpRows + (t & 7);
   if (c >= cols || r >= rows || v >= n_views) return;
@@ -253,9 +250,9 @@ template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                    const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
-                   float *__restrict__ out, unsigned zpitch, unsigned ystride, int rb0) {
-  fp_rays<VG, FIXS, false, COLS, PROBE>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch,
-                                        ystride, nullptr, rb0);
+                   float *__restrict__ out, unsigned zpitch, unsigned ystride) {
+  fp_rays<VG, FIXS, false, COLS, PROBE>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
+                                 nullptr);
 }
 
 // The same march storing into row-band destinations (tk_forward_cone_3d_bands).
@@ -273,7 +270,7 @@ template <int VG, int CPS, bool FIXS, int COLS = kFpCols>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_mirror_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                           const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
-                          float *__restrict__ out, unsigned zpitch, unsigned ystride, int /*rb0: always 0*/) {
+                          float *__restrict__ out, unsigned zpitch, unsigned ystride) {
   constexpr int SUB = COLS * kFpRows;
   const int half = (rows + 1) >> 1;  // direct rows [0, half); an odd detector's middle row is its own mirror
   const int ncb = (cols + COLS - 1) / COLS;
@@ -398,44 +395,6 @@ __global__ void __launch_bounds__(128)
   if (valid) out[((long long)v * rows + r) * cols + c] = live ? mine : 0.f;
 }
 
-// Per 8-row detector band: the volume z rows the taps of its samples can touch, over
-// every view and column (tk_fp_band_z, for upload-ordered pipelines).  Block = one
-// (view, band); samples at e + (k + 1/2) g lie between the first and the last sample,
-// whose taps are rows floor(z) - 1, floor(z) of the margin-1 padded coordinate z; one
-// row of slack on each side covers the fp32 march's rounding.
-__global__ void __launch_bounds__(256) fp_band_z_kernel(const ConeRayView *__restrict__ views, int n_views, int rows,
-                                                        int cols, int nx, int ny, int nz, double sx, double sy,
-                                                        double sz, double step, int *__restrict__ zlo,
-                                                        int *__restrict__ zhi) {
-  const int nbands = (rows + kFpRows - 1) / kFpRows;
-  const int v = (int)(blockIdx.x / nbands), band = (int)(blockIdx.x % nbands);
-  int lo = INT_MAX, hi = INT_MIN;
-  const int r0 = band * kFpRows, nr = min(kFpRows, rows - r0);
-  for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
-    const int r = r0 + i / cols, c = i % cols;
-    RaySetup rs;
-    if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) continue;
-    const double za = (double)rs.ez + 0.5 * (double)rs.gz;
-    const double zb = (double)rs.ez + ((double)(rs.n - 1) + 0.5 * (double)rs.last) * (double)rs.gz;
-    lo = min(lo, (int)floor(fmin(za, zb)) - 2);
-    hi = max(hi, (int)floor(fmax(za, zb)) + 1);
-  }
-  for (int o = 16; o; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  __shared__ int slo[8], shi[8];
-  if ((threadIdx.x & 31) == 0) slo[threadIdx.x >> 5] = lo, shi[threadIdx.x >> 5] = hi;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) lo = min(lo, slo[w]), hi = max(hi, shi[w]);
-    if (lo <= hi) {
-      atomicMin(zlo + band, max(lo, 0));
-      atomicMax(zhi + band, min(hi, nz - 1));
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -533,10 +492,9 @@ struct FpPlan {
   double sz = 0, sy = 0, sx = 0;
   FpLayout lay[2];             // [general, mirror]
   void *cells[2] = {nullptr, nullptr};
-  int cb0 = 0, cb1 = 0;        // padded-z cell range of the general layout built so far
 };
 
-static int plan_alloc(FpPlan &pl, bool mirror, cudaStream_t st) {
+static int plan_cells(FpPlan &pl, bool mirror, cudaStream_t st) {
   const int k = mirror ? 1 : 0;
   if (pl.cells[k]) return TK_OK;
   FpLayout &L = pl.lay[k];
@@ -554,47 +512,16 @@ static int plan_alloc(FpPlan &pl, bool mirror, cudaStream_t st) {
     pl.cells[k] = nullptr;
     return check_cuda(e, "cudaMallocAsync (forward-projection cells)");
   }
-  return TK_OK;
-}
-
-// general layout: build the cells of padded z in [lo, hi) not built yet (the built range
-// stays one interval: callers grow it outward from where it started)
-static int plan_build_z(FpPlan &pl, int lo, int hi, cudaStream_t st) {
-  const FpLayout &L = pl.lay[0];
-  auto launch = [&](int a, int b) -> int {
-    if (a >= b) return TK_OK;
-    dim3 g(ceil_div(b - a, 32), ceil_div(pl.nx + 2 * kFpMargin, 32), pl.ny + 2 * kFpMargin);
-    fp_cells_kernel<<<g, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, static_cast<float4 *>(pl.cells[0]), L.zpitch,
-                                       L.ystride, a, b);
-    TK_LAUNCHED("fp_cells_kernel");
-    return TK_OK;
-  };
-  int rc;
-  if (pl.cb0 >= pl.cb1) {
-    rc = launch(lo, hi);
-    pl.cb0 = lo, pl.cb1 = hi;
-    return rc;
-  }
-  rc = launch(lo, std::min(hi, pl.cb0));
-  if (rc == TK_OK) rc = launch(std::max(lo, pl.cb1), hi);
-  pl.cb0 = std::min(pl.cb0, lo), pl.cb1 = std::max(pl.cb1, hi);
-  return rc;
-}
-
-static int plan_cells(FpPlan &pl, bool mirror, cudaStream_t st) {
-  const int k = mirror ? 1 : 0;
-  const bool had = pl.cells[k] != nullptr;
-  int rc = plan_alloc(pl, mirror, st);
-  if (rc != TK_OK) return rc;
-  const FpLayout &L = pl.lay[k];
   if (mirror) {
-    if (had) return TK_OK;
     dim3 g(ceil_div(L.zcells, 32), ceil_div(pl.nx + 2 * kFpMargin, 32), pl.ny + 2 * kFpMargin);
     fp_mirror_cells_kernel<<<g, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, static_cast<float4 *>(pl.cells[k]),
                                               L.zpitch, L.ystride, L.zcells);
     TK_LAUNCHED("fp_mirror_cells_kernel");
   } else {
-    return plan_build_z(pl, 0, pl.nz + 2 * kFpMargin, st);  // whatever is not built yet
+    dim3 g(ceil_div(pl.nz + 2 * kFpMargin, 32), ceil_div(pl.nx + 2 * kFpMargin, 32), pl.ny + 2 * kFpMargin);
+    fp_cells_kernel<<<g, 256, 0, st>>>(pl.vol, pl.nz, pl.ny, pl.nx, static_cast<float4 *>(pl.cells[k]), L.zpitch,
+                                       L.ystride);
+    TK_LAUNCHED("fp_cells_kernel");
   }
   return TK_OK;
 }
@@ -608,7 +535,7 @@ static void plan_free(FpPlan &pl, cudaStream_t st) {
 }
 
 using FpKern = void (*)(const float4 *, int, int, int, double, double, double, const ConeRayView *, int, int, int,
-                        double, float *, unsigned, unsigned, int);
+                        double, float *, unsigned, unsigned);
 
 // Launch configurations (views per CTA x CTAs per SM): general 8x4 with 8-column view
 // tiles (default: 32 registers, 64 warps/SM; 420.6 vs 423.7 ms for 16-column tiles at
@@ -638,13 +565,10 @@ static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
          fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault> : cone_fp_kernel<8, 4, false, kFpColsDefault>;
 }
 
-// rows [row0, row1) only (row0 a multiple of 8) when row1 > 0: the general kernel from
-// whatever cells tk_fp_plan_cells built (all of them when none were built)
 static int plan_project(FpPlan &pl, const double *sources, const double *minv, int n_views, int rows, int cols,
-                        double step, float *out, cudaStream_t st, int row0 = 0, int row1 = 0) {
-  const bool ranged = row1 > 0;
-  const bool mirror = !ranged && fp_use_mirror(sources, minv, n_views, rows, pl.nz, pl.ny, pl.nx);
-  int rc = ranged && pl.cells[0] && pl.cb0 < pl.cb1 ? TK_OK : plan_cells(pl, mirror, st);
+                        double step, float *out, cudaStream_t st) {
+  const bool mirror = fp_use_mirror(sources, minv, n_views, rows, pl.nz, pl.ny, pl.nx);
+  int rc = plan_cells(pl, mirror, st);
   if (rc != TK_OK) return rc;
   const FpLayout &L = pl.lay[mirror ? 1 : 0];
   std::vector<ConeRayView> hv(n_views);
@@ -655,7 +579,7 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
   Scratch dviews;
   TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
   const char *algo = getenv("TK_FP_ALGO");
-  if (!mirror && !ranged && algo && !strcmp(algo, "warp")) {  // warp-cooperative comparison kernel
+  if (!mirror && algo && !strcmp(algo, "warp")) {  // warp-cooperative comparison kernel
     const long long nbw = (long long)ceil_div(cols, kFpCols) * ceil_div(rows, kFpRows) * n_views;
     if (nbw >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
     auto kw = L.fixs ? cone_fp_warp_kernel<true> : cone_fp_warp_kernel<false>;
@@ -668,13 +592,11 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
   int vg = 1, tcols = kFpCols;
   FpKern kern = pick_kernel(mirror, L.fixs, vg, tcols);
   const int brows = mirror ? (rows + 1) / 2 : rows;
-  const int rb0 = ranged ? row0 / kFpRows : 0;
-  const int nrb = ranged ? ceil_div(row1, kFpRows) - rb0 : ceil_div(brows, kFpRows);
-  const long long nb = (long long)ceil_div(cols, tcols) * nrb * ceil_div(n_views, vg);
+  const long long nb = (long long)ceil_div(cols, tcols) * ceil_div(brows, kFpRows) * ceil_div(n_views, vg);
   if (nb >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
-  kern<<<(unsigned)nb, tcols * kFpRows * vg, 0, st>>>(static_cast<const float4 *>(pl.cells[mirror ? 1 : 0]), pl.nx,
-                                                      pl.ny, pl.nz, pl.sx, pl.sy, pl.sz, dviews.as<ConeRayView>(),
-                                                      rows, cols, n_views, step, out, L.zpitch, L.ystride, rb0);
+  kern<<<(unsigned)nb, tcols * kFpRows * vg, 0, st>>>(static_cast<const float4 *>(pl.cells[mirror ? 1 : 0]), pl.nx, pl.ny, pl.nz,
+                                          pl.sx, pl.sy, pl.sz, dviews.as<ConeRayView>(), rows, cols, n_views, step, out,
+                                          L.zpitch, L.ystride);
   TK_LAUNCHED(mirror ? "cone_fp_mirror_kernel" : "cone_fp_kernel");
   return TK_OK;
 }
@@ -761,70 +683,6 @@ int tk_fp_plan_project(void *plan, const double *sources, const double *minv, in
   if (n_views < 1 || rows < 1 || cols < 1 || !(step > 0)) return fail_arg("tk_fp_plan_project: bad extent / step");
   return plan_project(*reinterpret_cast<FpPlan *>(plan), sources, minv, n_views, rows, cols, step, out,
                       as_stream(stream));
-}
-
-int tk_fp_plan_cells(void *plan, int z0, int z1, void *stream) {
-  clear_error();
-  if (!plan) return fail_arg("tk_fp_plan_cells: null plan");
-  FpPlan &pl = *reinterpret_cast<FpPlan *>(plan);
-  if (z0 < 0 || z1 > pl.nz || z0 >= z1) return fail_arg("tk_fp_plan_cells: need 0 <= z0 < z1 <= nz");
-  const cudaStream_t st = as_stream(stream);
-  int rc = plan_alloc(pl, false, st);
-  if (rc != TK_OK) return rc;
-  constexpr int m = kFpMargin;
-  // cells of padded z hold volume rows z - m and z - m + 1: computable when each is in
-  // [z0, z1) or outside the volume (zero margin)
-  const int lo = z0 == 0 ? 0 : z0 + m, hi = z1 == pl.nz ? pl.nz + 2 * m : z1 + m - 1;
-  if (pl.cb0 < pl.cb1 && (hi < pl.cb0 || lo > pl.cb1))
-    return fail_arg("tk_fp_plan_cells: ranges must grow one interval");
-  return plan_build_z(pl, lo, hi, st);
-}
-
-int tk_fp_plan_project_rows(void *plan, const double *sources, const double *minv, int n_views, int rows, int cols,
-                            int row0, int row1, double step, float *out, void *stream) {
-  clear_error();
-  if (!plan || !sources || !minv || !out) return fail_arg("tk_fp_plan_project_rows: null pointer");
-  if (n_views < 1 || rows < 1 || cols < 1 || !(step > 0))
-    return fail_arg("tk_fp_plan_project_rows: bad extent / step");
-  if (row0 < 0 || row0 >= row1 || row1 > rows || row0 % kFpRows || (row1 % kFpRows && row1 != rows))
-    return fail_arg("tk_fp_plan_project_rows: rows [row0, row1) must be whole 8-row bands");
-  return plan_project(*reinterpret_cast<FpPlan *>(plan), sources, minv, n_views, rows, cols, step, out,
-                      as_stream(stream), row0, row1);
-}
-
-int tk_fp_band_z(const double *sources, const double *minv, int n_views, int rows, int cols, int nz, int ny, int nx,
-                 double sz, double sy, double sx, double step, int *zlo, int *zhi, void *stream) {
-  clear_error();
-  if (!sources || !minv || !zlo || !zhi) return fail_arg("tk_fp_band_z: null pointer");
-  if (n_views < 1 || rows < 1 || cols < 1 || nz < 1 || ny < 1 || nx < 1 || !(step > 0))
-    return fail_arg("tk_fp_band_z: bad extent / step");
-  const cudaStream_t st = as_stream(stream);
-  const int nbands = ceil_div(rows, kFpRows);
-  std::vector<ConeRayView> hv(n_views);
-  for (int i = 0; i < n_views; ++i) {
-    for (int j = 0; j < 3; ++j) hv[i].src[j] = sources[3 * i + j];
-    for (int j = 0; j < 9; ++j) hv[i].minv[j] = minv[9 * i + j];
-  }
-  std::vector<int> init(2 * (size_t)nbands);
-  for (int b = 0; b < nbands; ++b) init[b] = INT_MAX, init[nbands + b] = INT_MIN;
-  Scratch dviews, dz;
-  TK_TRY_CUDA(upload(dviews, hv.data(), sizeof(ConeRayView) * n_views, st));
-  TK_TRY_CUDA(upload(dz, init.data(), sizeof(int) * init.size(), st));
-  int *d = dz.as<int>();
-  fp_band_z_kernel<<<(unsigned)((long long)n_views * nbands), 256, 0, st>>>(
-      dviews.as<ConeRayView>(), n_views, rows, cols, nx, ny, nz, sx, sy, sz, step, d, d + nbands);
-  TK_LAUNCHED("fp_band_z_kernel");
-  TK_TRY_CUDA(cudaMemcpyAsync(init.data(), d, sizeof(int) * init.size(), cudaMemcpyDeviceToHost, st));
-  TK_TRY_CUDA(cudaStreamSynchronize(st));
-  for (int b = 0; b < nbands; ++b) zlo[b] = init[b], zhi[b] = init[nbands + b];
-  return TK_OK;
-}
-
-int tk_copy_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height, void *stream) {
-  clear_error();
-  if (!dst || !src) return fail_arg("tk_copy_2d: null pointer");
-  TK_TRY_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, as_stream(stream)));
-  return TK_OK;
 }
 
 int tk_fp_plan_destroy(void *plan, void *stream) {

@@ -159,30 +159,6 @@ def forward_kernel_path(geom: GeometryCone3D) -> str:
         else "general"
 
 
-FP_BAND_ROWS = 8  # detector rows per band of the forward projector's launches (tk_fp.cu kFpRows)
-
-
-def band_z_extent(geom: GeometryCone3D, step: float) -> np.ndarray:
-    """(n_bands, 2) int array: for each 8-row detector band, the first and last volume z row
-    the taps of its samples can touch over every view and column (tk_fp_band_z; first >
-    last when no ray of the band meets the volume).  Computed on the device once per
-    geometry and step."""
-    cache = geom.__dict__.setdefault("_band_z_cache", {})
-    key = float(step)
-    if key not in cache:
-        src, minv = geom.ray_constants
-        (src, psrc), (minv, pminv) = _lib.host_f64(src), _lib.host_f64(minv)
-        rows, cols = geom.detector_shape
-        nz, ny, nx = geom.volume_shape
-        sz, sy, sx = geom.volume_spacing
-        nb = -(-rows // FP_BAND_ROWS)
-        lo, hi = (ctypes.c_int * nb)(), (ctypes.c_int * nb)()
-        _lib.call("tk_fp_band_z", psrc, pminv, src.shape[0], rows, cols, nz, ny, nx, sz, sy, sx, key, lo, hi,
-                  _lib.stream_ptr())
-        cache[key] = np.stack([np.frombuffer(lo, dtype=np.int32), np.frombuffer(hi, dtype=np.int32)], 1).copy()
-    return cache[key]
-
-
 class ForwardProjectionPlan:
     """A cone-beam volume prepared once (tk_fp_plan_create) and projected in
     view blocks (tk_fp_plan_project) -- used to overlap per-block D2H copies
@@ -212,25 +188,6 @@ class ForwardProjectionPlan:
         with torch.cuda.device(self.device):
             _lib.call("tk_fp_plan_project", self._handle, psrc, pminv, src.shape[0], rows, cols,
                       float(step), _lib.dev_ptr(out), _lib.stream_ptr(self.device))
-        return out
-
-    def cells(self, z0: int, z1: int) -> None:
-        """Volume rows [z0, z1) are on the device (one growing contiguous range): build
-        the cells computable from them on the current stream (tk_fp_plan_cells)."""
-        with torch.cuda.device(self.device):
-            _lib.call("tk_fp_plan_cells", self._handle, int(z0), int(z1), _lib.stream_ptr(self.device))
-
-    def project_rows(self, row0: int, row1: int, out: torch.Tensor, step: float) -> torch.Tensor:
-        """Detector rows [row0, row1) (whole 8-row bands) of every view into the full
-        (views, rows, cols) sinogram `out`, from the cells built so far."""
-        src, minv = self.geom.ray_constants
-        (src, psrc), (minv, pminv) = _lib.host_f64(src), _lib.host_f64(minv)
-        rows, cols = self.geom.detector_shape
-        if tuple(out.shape) != (src.shape[0], rows, cols) or not out.is_contiguous():
-            raise ValueError("plan output must be the contiguous (views, rows, cols) sinogram")
-        with torch.cuda.device(self.device):
-            _lib.call("tk_fp_plan_project_rows", self._handle, psrc, pminv, src.shape[0], rows, cols, int(row0),
-                      int(row1), float(step), _lib.dev_ptr(out), _lib.stream_ptr(self.device))
         return out
 
     def close(self) -> None:
