@@ -171,7 +171,7 @@ struct FpDests {
 // PROBE (roofline decomposition, TK_FP_PROBE; not a projector): 1 = the march with its
 // cell loads but a 1-FADD "interpolation" (the access stream alone), 2 = the full
 // arithmetic on cell values synthesised from the cell index instead of loaded.
-template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0>
+template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
@@ -206,6 +206,7 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
   const float magic = 8388608.f;  // coordinates >= 0: floor(f) = bits(f + 2^23) - 0x4B000000
   const unsigned sys = FIXS ? kFpFixS : ystride;
+  const unsigned zp = ZP ? (unsigned)ZP : zpitch;  // compile-time z pitch (fixed stride, nz + 4 <= 1023)
   const unsigned long long e2 = pk2(ex, ey), g2 = pk2(rs.gx, rs.gy), m2 = pk2(magic, magic);
   const float gz = rs.gz;
   unsigned cell = 0xffffffffu;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
     const unsigned long long xxy = fadd2_rm(fxy, m2);
     const float xz = __fadd_rd(fz, magic);
     const float2 xb = upk2(xxy);
-    const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zpitch + __float_as_uint(xz));
+    const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zp + __float_as_uint(xz));
     if (id != cell) {
       cell = id;
       if (PROBE == 2) {
@@ -246,12 +247,12 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   store(acc * (float)step);
 }
 
-template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0>
+template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0, int ZP = 0>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                    const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                    float *__restrict__ out, unsigned zpitch, unsigned ystride) {
-  fp_rays<VG, FIXS, false, COLS, PROBE>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
+  fp_rays<VG, FIXS, false, COLS, PROBE, ZP>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
                                  nullptr);
 }
 
@@ -541,7 +542,7 @@ using FpKern = void (*)(const float4 *, int, int, int, double, double, double, c
 // tiles (default: 32 registers, 64 warps/SM; 420.6 vs 423.7 ms for 16-column tiles at
 // 8x2, profiles/r02/fp_ab_r02ap.log), 8x2 or 4x4 with 16-column tiles; mirror 4x3
 // (default, 40 registers), 8x2, 8x1.
-static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
+static FpKern pick_kernel(bool mirror, bool fixs, unsigned zpitch, int &vg, int &tcols) {
   tcols = kFpCols;
   const char *ce = getenv("TK_FP_CFG");
   const bool c8x1 = ce && !strcmp(ce, "8x1"), c8x2 = ce && !strcmp(ce, "8x2"), c4x4 = ce && !strcmp(ce, "4x4"),
@@ -561,6 +562,14 @@ static FpKern pick_kernel(bool mirror, bool fixs, int &vg, int &tcols) {
            fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 2> : cone_fp_kernel<8, 4, false, kFpColsDefault, 2>;
   if (c8x2) return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
+  if (fixs && env_int("TK_FP_ZP", 1)) {  // the fixed layout's z pitch as an immediate
+    constexpr int C = kFpColsDefault;
+    vg = 8, tcols = C;
+    if (zpitch == 255) return cone_fp_kernel<8, 4, true, C, 0, 255>;
+    if (zpitch == 511) return cone_fp_kernel<8, 4, true, C, 0, 511>;
+    if (zpitch == 767) return cone_fp_kernel<8, 4, true, C, 0, 767>;
+    if (zpitch == 1023) return cone_fp_kernel<8, 4, true, C, 0, 1023>;
+  }
   return vg = 8, tcols = kFpColsDefault,
          fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault> : cone_fp_kernel<8, 4, false, kFpColsDefault>;
 }
@@ -590,7 +599,7 @@ static int plan_project(FpPlan &pl, const double *sources, const double *minv, i
     return TK_OK;
   }
   int vg = 1, tcols = kFpCols;
-  FpKern kern = pick_kernel(mirror, L.fixs, vg, tcols);
+  FpKern kern = pick_kernel(mirror, L.fixs, L.zpitch, vg, tcols);
   const int brows = mirror ? (rows + 1) / 2 : rows;
   const long long nb = (long long)ceil_div(cols, tcols) * ceil_div(brows, kFpRows) * ceil_div(n_views, vg);
   if (nb >= (1LL << 31)) return fail_arg("tk_forward_cone_3d: problem too large for one launch");
