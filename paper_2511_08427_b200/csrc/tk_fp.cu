@@ -171,7 +171,7 @@ struct FpDests {
 // PROBE (roofline decomposition, TK_FP_PROBE; not a projector): 1 = the march with its
 // cell loads but a 1-FADD "interpolation" (the access stream alone), 2 = the full
 // arithmetic on cell values synthesised from the cell index instead of loaded.
-template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0>
+template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0, bool MOVE_FREE = true>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
@@ -218,8 +218,9 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
     const float xz = __fadd_rd(fz, magic);
     const float2 xb = upk2(xxy);
     const unsigned id = __float_as_uint(xb.y) * sys + (__float_as_uint(xb.x) * zp + __float_as_uint(xz));
-    if (id != cell) {
-      cell = id;
+    const bool changed = id != cell;
+    if (!MOVE_FREE) cell = changed ? id : cell;
+    if (changed) {
       if (PROBE == 2) {
         lo4.x = __uint_as_float((id & 0x7fffu) | 0x3f800000u);
         lo4 = make_float4(lo4.x, lo4.x, lo4.x, lo4.x);
@@ -230,6 +231,7 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
         hi4 = __ldg(p + sys);
       }
     }
+    if (MOVE_FREE) cell = id;  // == the cell of the last load: no predicated move, renamed by the unroll
     if (PROBE == 1) return lo4.x + hi4.w;
     const float2 w = upk2(fsub2(fxy, fsub2(xxy, m2)));
     const float wz = fz - (xz - magic);
