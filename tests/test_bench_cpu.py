@@ -45,3 +45,26 @@ def test_roofline_names_the_binding_bound():
     assert r["hbm"]["algorithmic_bytes_per_launch"] == alg
     assert r["hbm"]["frac"] == pytest.approx(alg / 1.0 / 1e9 / r["hbm"]["peak"], rel=1e-2)
     assert r["back"]["frac"] == pytest.approx(16.0e11 / 0.1 / 1e9 / 36000.0, rel=1e-3)
+
+
+def test_ncu_traffic_takes_the_newest_capture(tmp_path, monkeypatch):
+    """The roofline's `traffic` comes from the newest committed cfg4 capture: round-letter
+    order (r02aq after r02k), and a capture of a view-subset launch is scaled to the
+    whole call the bench times."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    prof = tmp_path / "profiles" / "r02"
+    prof.mkdir(parents=True)
+    k = bench.FP_KERNEL
+    (prof / "ncu_r02k_old.json").write_text(json.dumps({k: {"dram_bytes_per_launch": 1.0, "config": "cfg4-full"}}))
+    (prof / "ncu_r02aq_new.json").write_text(json.dumps({k: {"dram_bytes_per_launch": 2.0, "config": "cfg4-full"}}))
+    (prof / "ncu_r02zz_probe.json").write_text(json.dumps({k: {"dram_bytes_per_launch": 9.0,
+                                                               "config": "cfg4-probe1"}}))
+    (prof / "ncu_r02ap_bp.json").write_text(json.dumps({"bpk": {"dram_bytes_per_launch": 3.0, "views": 360,
+                                                                 "config": "cfg4-full"}}))
+    monkeypatch.setattr(bench, "ROOT", tmp_path)
+    traffic, src = bench.ncu_traffic(k)
+    assert traffic == 2.0 and src.endswith("ncu_r02aq_new.json")
+    traffic, _ = bench.ncu_traffic("bpk")
+    assert traffic == 3.0 * bench.VIEWS / 360
