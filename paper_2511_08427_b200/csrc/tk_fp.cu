@@ -171,7 +171,8 @@ struct FpDests {
 // PROBE (roofline decomposition, TK_FP_PROBE; not a projector): 1 = the march with its
 // cell loads but a 1-FADD "interpolation" (the access stream alone), 2 = the full
 // arithmetic on cell values synthesised from the cell index instead of loaded.
-template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0, bool MOVE_FREE = true>
+template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0, bool MOVE_FREE = true,
+          int UNR = 2>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
                                         double sz, const ConeRayView *__restrict__ views, int rows, int cols,
                                         int n_views, double step, float *__restrict__ out, unsigned zpitch,
@@ -243,18 +244,23 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   float acc = 0.f;
   float kf = 0.5f;
   const int nfull = rs.n - 1;
+  if (UNR == 3) {  // the default launch: 415.95 vs 417.31 ms at unroll 2 (1: 422.6, 4: 437.6, spills)
+#pragma unroll 3
+    for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+  } else {
 #pragma unroll 2
-  for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+    for (int k = 0; k < nfull; ++k, kf += 1.f) acc += sample(kf);
+  }
   acc = fmaf(rs.last, sample((float)nfull + 0.5f * rs.last), acc);  // exact last segment
   store(acc * (float)step);
 }
 
-template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0, int ZP = 0>
+template <int VG, int CPS, bool FIXS, int COLS = kFpCols, int PROBE = 0, int ZP = 0, int UNR = 2>
 __global__ void __launch_bounds__(COLS * kFpRows * VG, CPS)
     cone_fp_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                    const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                    float *__restrict__ out, unsigned zpitch, unsigned ystride) {
-  fp_rays<VG, FIXS, false, COLS, PROBE, ZP>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
+  fp_rays<VG, FIXS, false, COLS, PROBE, ZP, true, UNR>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, out, zpitch, ystride,
                                  nullptr);
 }
 
@@ -567,13 +573,14 @@ static FpKern pick_kernel(bool mirror, bool fixs, unsigned zpitch, int &vg, int 
   if (fixs && env_int("TK_FP_ZP", 1)) {  // the fixed layout's z pitch as an immediate
     constexpr int C = kFpColsDefault;
     vg = 8, tcols = C;
-    if (zpitch == 255) return cone_fp_kernel<8, 4, true, C, 0, 255>;
-    if (zpitch == 511) return cone_fp_kernel<8, 4, true, C, 0, 511>;
-    if (zpitch == 767) return cone_fp_kernel<8, 4, true, C, 0, 767>;
-    if (zpitch == 1023) return cone_fp_kernel<8, 4, true, C, 0, 1023>;
+    if (zpitch == 255) return cone_fp_kernel<8, 4, true, C, 0, 255, 3>;
+    if (zpitch == 511) return cone_fp_kernel<8, 4, true, C, 0, 511, 3>;
+    if (zpitch == 767 && env_int("TK_FP_UNR", 3) == 2) return cone_fp_kernel<8, 4, true, C, 0, 767, 2>;
+    if (zpitch == 767) return cone_fp_kernel<8, 4, true, C, 0, 767, 3>;
+    if (zpitch == 1023) return cone_fp_kernel<8, 4, true, C, 0, 1023, 3>;
   }
   return vg = 8, tcols = kFpColsDefault,
-         fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault> : cone_fp_kernel<8, 4, false, kFpColsDefault>;
+         fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 0, 0, 3> : cone_fp_kernel<8, 4, false, kFpColsDefault, 0, 0, 3>;
 }
 
 static int plan_project(FpPlan &pl, const double *sources, const double *minv, int n_views, int rows, int cols,

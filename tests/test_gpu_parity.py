@@ -756,7 +756,8 @@ def test_nondeterministic_transposes_follow_torch_determinism(tk):
     bp_adjoint_tensor(x, geom)  # fine when the switch is off
 
 
-@pytest.mark.parametrize("knobs", [{"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x2"}, {"TK_FP_ZP": "0"}, {"TK_FP_NOFIX": "1"},
+@pytest.mark.parametrize("knobs", [{"TK_FP_CFG": "4x4"}, {"TK_FP_CFG": "8x2"}, {"TK_FP_ZP": "0"}, {"TK_FP_UNR": "2"},
+                                   {"TK_FP_NOFIX": "1"},
                                    {"TK_FP_MIRROR": "1"}, {"TK_FP_MIRROR": "1", "TK_FP_NOFIX": "1"},
                                    {"TK_FP_MIRROR": "1", "TK_FP_CFG": "8x1"}, {"TK_FP_MIRROR": "1", "TK_FP_CFG": "8x2"}])
 def test_fp_tuning_knobs_keep_results(tk, monkeypatch, knobs):
