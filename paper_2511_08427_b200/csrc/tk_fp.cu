@@ -270,8 +270,8 @@ __global__ void __launch_bounds__(kFpColsDefault * kFpRows * 8, 4)
     cone_fp_bands_kernel(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy, double sz,
                          const ConeRayView *__restrict__ views, int rows, int cols, int n_views, double step,
                          unsigned zpitch, unsigned ystride, const __grid_constant__ FpDests dests) {
-  fp_rays<8, FIXS, true, kFpColsDefault>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step, nullptr, zpitch,
-                                         ystride, &dests);
+  fp_rays<8, FIXS, true, kFpColsDefault, 0, 0, true, 3>(q, nx, ny, nz, sx, sy, sz, views, rows, cols, n_views, step,
+                                                        nullptr, zpitch, ystride, &dests);
 }
 
 // Sub-block = 16 columns x 8 direct rows (lower detector half) plus their 8 mirror rows.
