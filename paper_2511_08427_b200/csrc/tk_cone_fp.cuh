@@ -33,7 +33,8 @@ struct RaySetup {
 __device__ __forceinline__ bool clip_axis(double p, double d, double h, double &t0,
                                           double &t1, int axis, int &face) {
   if (fabs(d) > kTiny) {
-    double ta = (-h - p) / d, tb = (h - p) / d;
+    const double rd = 1.0 / d;  // one fp64 division per axis instead of two
+    double ta = (-h - p) * rd, tb = (h - p) * rd;
     const double tn = fmin(ta, tb);
     if (tn > t0) face = axis;
     t0 = fmax(t0, tn);
@@ -50,7 +51,7 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
   double dx = V.minv[0] * c + V.minv[1] * r + V.minv[2];
   double dy = V.minv[3] * c + V.minv[4] * r + V.minv[5];
   double dz = V.minv[6] * c + V.minv[7] * r + V.minv[8];
-  double inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+  double inv = rsqrt(dx * dx + dy * dy + dz * dz);
   dx *= inv;
   dy *= inv;
   dz *= inv;

@@ -170,7 +170,8 @@ struct FpDests {
 
 // PROBE (roofline decomposition, TK_FP_PROBE; not a projector): 1 = the march with its
 // cell loads but a 1-FADD "interpolation" (the access stream alone), 2 = the full
-// arithmetic on cell values synthesised from the cell index instead of loaded.
+// arithmetic on cell values synthesised from the cell index instead of loaded,
+// 7 = the per-ray float64 set-up alone.
 template <int VG, bool FIXS, bool BANDS, int COLS = kFpCols, int PROBE = 0, int ZP = 0, bool MOVE_FREE = true,
           int UNR = 2>
 __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, int ny, int nz, double sx, double sy,
@@ -202,6 +203,10 @@ __device__ __forceinline__ void fp_rays(const float4 *__restrict__ q, int nx, in
   RaySetup rs;
   if (!cone_ray_setup(views[v], r, c, nx, ny, nz, sx, sy, sz, step, rs)) {
     store(0.f);
+    return;
+  }
+  if (PROBE == 7) {  // per-ray set-up only (its share of the projector's time)
+    store(rs.ex + rs.gz * (float)rs.n + rs.last);
     return;
   }
   const float ex = rs.ex + (kFpMargin - 1), ey = rs.ey + (kFpMargin - 1), ez = rs.ez + (kFpMargin - 1);
@@ -568,6 +573,10 @@ static FpKern pick_kernel(bool mirror, bool fixs, unsigned zpitch, int &vg, int 
   if (probe == 2)
     return vg = 8, tcols = kFpColsDefault,
            fixs ? cone_fp_kernel<8, 4, true, kFpColsDefault, 2> : cone_fp_kernel<8, 4, false, kFpColsDefault, 2>;
+  if (probe == 7 && fixs && zpitch == 767) {
+    vg = 8, tcols = kFpColsDefault;
+    return cone_fp_kernel<8, 4, true, kFpColsDefault, 7, 767, 3>;
+  }
   if (c8x2) return vg = 8, fixs ? cone_fp_kernel<8, 2, true> : cone_fp_kernel<8, 2, false>;
   if (c4x4 || c4x3) return vg = 4, fixs ? cone_fp_kernel<4, 4, true> : cone_fp_kernel<4, 4, false>;
   if (fixs && env_int("TK_FP_ZP", 1)) {  // the fixed layout's z pitch as an immediate
