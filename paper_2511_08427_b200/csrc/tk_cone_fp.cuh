@@ -64,10 +64,11 @@ __device__ __forceinline__ bool cone_ray_setup(const ConeRayView &V, int r, int 
   if (!clip_axis(pz, dz, (nz + 1) * sz / 2.0, t0, t1, 2, face)) return false;
   if (!(t0 < t1)) return false;
   // _kernels.py:133: while t < t1 - TINY  ->  n = ceil((t1 - TINY - t0) / step)
-  double span = (t1 - kTiny - t0) / step;
+  const double istep = 1.0 / step;
+  double span = (t1 - kTiny - t0) * istep;
   if (!(span > 0.0)) return false;
   int n = (int)ceil(span);
-  double last = (t1 - t0) / step - (double)(n - 1);
+  double last = (t1 - t0) * istep - (double)(n - 1);
   if (last > 1.0) last = 1.0;
   // padded-index coordinates (centre (n-1)/2 + 1, _kernels.py:122-124, 138-140)
   const double cx = (nx - 1) / 2.0 + 1.0, cy = (ny - 1) / 2.0 + 1.0, cz = (nz - 1) / 2.0 + 1.0;
